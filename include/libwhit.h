@@ -1,0 +1,165 @@
+/*
+ * libwhit -- B200 (sm_100a) hot path of the differentiable heteroscedastic
+ * Whittaker layer, arXiv 2604.00048 ("the paper"; PAPER.md line n = P:n).
+ *
+ * For B independent series of length T (the paper's pixel time series)
+ * the library solves, per series,
+ *
+ *     Omega z = W y,   Omega = W + D^T diag(lambda) D             Eq. (3)
+ *
+ * where W = diag(w) holds observation weights (1 observed, 0 cloud / gap /
+ * padding), D is the order-d difference operator (the paper's order
+ * k+1; on the daily grid its rows are the binomial stencil
+ * c_j = (-1)^(d-j) C(d,j)), and lambda holds one penalty weight per
+ * difference row -- or one scalar per series, the homoscedastic
+ * Eq. (2).  Omega is symmetric positive definite with bandwidth d
+ * and is factored by banded LDL^T with forward and back substitution
+ * (Algorithm 1 P:127-142 is the LL^T analogue) -- never materialised:
+ * each row of the band is assembled in registers from w, lambda and D.
+ *
+ * The backward pass takes the upstream cotangent g = dL/dz, solves
+ * ONE adjoint system u = Omega^{-1} g with the same factor, and returns
+ *     dL/dy         = w * u                        Eq. (5), P:77 (as a VJP)
+ *     dL/dlambda_r  = -(D u)_r (D z)_r             Eq. (4), contracted with g
+ *     (scalar lambda: the sum over r).
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions shared by every entry point
+ * ---------------------------------------------------------------------------
+ * Pointers.  Every data pointer is a CUDA DEVICE pointer (cudaMalloc'd or a
+ *   torch CUDA tensor's data_ptr), 16-byte aligned.  The library never
+ *   allocates, frees, or copies through the host except where stated.
+ * Layout.  Time-outer, series-contiguous ("[T][B]"): element (t, b) of a
+ *   series-length plane lives at index t*B + b.  Planes: y, w, z, grad_z,
+ *   grad_y are [T][B]; per-date lambda and its gradient are [T-d][B]
+ *   (lambda_r weights difference row r, whose stencil covers dates r..r+d);
+ *   scalar lambda and its gradient are [B].
+ * Element type.  Either all planes are float32 (WHIT_F32) or all are float64
+ *   (WHIT_F64), fixed at workspace creation.  All arithmetic is fp64 in
+ *   registers either way; float32 outputs are rounded once at the store.
+ * Sizes.  1 <= d <= 3;  T >= d + 1;  1 <= B;  B % 4 == 0 (F32) or B % 2 == 0
+ *   (F64) so every time row is 16-byte aligned (the TMA row-stride rule);
+ *   T * B < 2^31 per plane row index range is NOT required (64-bit indexing).
+ * Inputs.  y finite where w > 0 (values where w == 0 are never read into the
+ *   arithmetic: (W y)_t := 0 there, so NaN padding is allowed); w >= 0 and
+ *   finite; lambda >= 0 and finite.  Inputs are never modified; outputs must
+ *   not alias inputs.
+ * Streams.  Every call is asynchronous on the stream bound to the workspace
+ *   (whit_ws_create / whit_ws_set_stream); nothing synchronises except
+ *   whit_failures.
+ * Errors.  Argument problems are detected on the host before any launch and
+ *   returned as a whit_status (nothing is launched); a launch failure returns
+ *   WHIT_ERR_CUDA.  whit_last_error() gives a one-line reason for the calling
+ *   thread's last non-OK status.  No C++ exception crosses this ABI.
+ * Numerical failure.  A series whose Omega is not SPD is NOT a call error:
+ *   the call returns WHIT_OK, that series' outputs (z, and in the backward
+ *   grad_y, grad_lambda) are NaN, and its status is recorded LAPACK-style
+ *   (xPBTRF "info") in the workspace: info[b] = 0 success; T-d+1 if fewer
+ *   than d days have w > 0 (Omega = W + D^T Lambda D is then singular for
+ *   lambda > 0: a nonzero polynomial of degree < d vanishing on every
+ *   observed day has zero objective); otherwise t+1 for the first pivot
+ *   D_t <= 0 or non-finite.  Read it with whit_failures().
+ */
+#ifndef LIBWHIT_H
+#define LIBWHIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LIBWHIT_VERSION 100 /* 1.0.0 */
+
+typedef enum {
+  WHIT_OK = 0,
+  WHIT_ERR_ARG = 1,    /* null pointer, bad enum, d out of range            */
+  WHIT_ERR_SHAPE = 2,  /* T, B inconsistent with the workspace or rules     */
+  WHIT_ERR_ALIGN = 3,  /* pointer not 16-B aligned or B % 4 (F32) / 2 (F64) */
+  WHIT_ERR_WS = 4,     /* workspace buffer missing or too small             */
+  WHIT_ERR_CUDA = 5,   /* CUDA runtime / driver error (see whit_last_error) */
+  WHIT_ERR_STATE = 6   /* backward without a matching forward, z mismatch   */
+} whit_status;
+
+typedef enum { WHIT_F32 = 0, WHIT_F64 = 1 } whit_dtype;
+
+typedef enum {
+  WHIT_LAMBDA_SCALAR = 0,   /* lambda is [B]: Eq. (2)           */
+  WHIT_LAMBDA_PER_DATE = 1  /* lambda is [T-d][B]: Eq. (3)  */
+} whit_lambda_mode;
+
+/* Opaque HOST handle describing one (d, T, B, dtype, lambda mode) problem and
+ * binding a caller-owned device buffer ("factor_ws").  It owns no device
+ * memory.  It carries the state a forward leaves for its backward: the
+ * factor checkpoints, the cached D z plane, the per-series info, and the
+ * w / lambda pointers of that forward. */
+typedef struct whit_ws whit_ws;
+
+/* Library version (LIBWHIT_VERSION). */
+int whit_version(void);
+
+/* Human-readable name of a status code (static string). */
+const char* whit_status_string(whit_status s);
+
+/* One-line reason for the calling thread's most recent non-OK status, or ""
+ * (thread-local static string, valid until the next call on that thread). */
+const char* whit_last_error(void);
+
+/* Bytes of device memory whit_ws_create needs for this problem; 0 if the
+ * arguments are invalid.  Host-only, no CUDA call.  Contents: the D z cache
+ * ([T-d][B] of the I/O dtype), fp64 factor checkpoints every K time steps
+ * (the forward's factor + RHS state, the backward's RHS state), and int32
+ * info[B]. */
+size_t whit_ws_bytes(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode);
+
+/* Create a workspace handle over dev_buf (device memory of at least
+ * whit_ws_bytes(...) bytes, 256-B aligned, owned by the caller and kept alive
+ * until whit_ws_destroy).  cuda_stream is a cudaStream_t (NULL = legacy
+ * default stream).  On success *out receives the handle. */
+whit_status whit_ws_create(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
+                           whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes,
+                           void* cuda_stream);
+
+/* Rebind the stream later calls launch on (cudaStream_t). */
+whit_status whit_ws_set_stream(whit_ws* ws, void* cuda_stream);
+
+/* Destroy the host handle (does not touch device memory).  NULL is a no-op. */
+void whit_ws_destroy(whit_ws* ws);
+
+/* Forward, Eq. (3) or Eq. (2):  z = (W + D^T diag(lambda) D)^{-1} W y.
+ *   y       [T][B]            observations (paper's x)
+ *   w       [T][B]            weights, diag of W
+ *   lambda  [T-d][B] or [B]   per the workspace's lambda mode
+ *   d, T, B                   must equal the workspace's
+ *   z       [T][B]            output
+ *   factor_ws                 receives the state the backward reuses; w and
+ *                             lambda must stay valid and unmodified until the
+ *                             matching whit_backward has run.
+ * One kernel launch. */
+whit_status whit_forward(const void* y, const void* w, const void* lambda, int d, int64_t T,
+                         int64_t B, void* z, whit_ws* factor_ws);
+
+/* Backward: one adjoint solve u = Omega^{-1} grad_z reusing the
+ * forward's factor (checkpointed in factor_ws, recomputed per chunk), then
+ *   grad_y      [T][B]             = w * u                       Eq. (5)
+ *   grad_lambda [T-d][B] or [B]    = -(D u)_r (D z)_r (or sum_r)   Eq. (4)
+ * z may be NULL; if non-NULL it must be the z pointer of the matching
+ * whit_forward (the cached fp64-derived D z is used, not z itself).
+ * Returns WHIT_ERR_STATE if no forward ran on factor_ws.  One kernel launch. */
+whit_status whit_backward(const void* grad_z, whit_ws* factor_ws, const void* z, void* grad_y,
+                          void* grad_lambda);
+
+/* SYNCHRONISES the workspace stream, then reports how many series of the
+ * last forward failed (non-SPD, see "Numerical failure") in *n_failed and,
+ * if host_info is non-NULL, copies info[0..B) (int32) to host_info. */
+whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info);
+
+/* Device pointer to the workspace's info[B] (int32), for callers that want to
+ * consume it on the device without a synchronisation. */
+const int32_t* whit_info_device(const whit_ws* ws);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBWHIT_H */

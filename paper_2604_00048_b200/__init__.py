@@ -1,0 +1,25 @@
+"""paper_2604_00048_b200 -- B200-native hot path of the differentiable
+heteroscedastic Whittaker layer (arXiv 2604.00048).
+
+The compute lives in ``libwhit.so`` (hand-written sm_100a CUDA behind the C-ABI
+of ``include/libwhit.h``); this package is the thin binding:
+
+* ``_lib``      ctypes marshalling for every C entry point (same names);
+* ``autograd``  ``WhittakerFn`` / ``smooth`` -- the torch autograd shim.
+
+Importing fails loudly (ImportError) when the shared library is missing.
+"""
+from ._lib import (  # noqa: F401
+    WHIT_F32,
+    WHIT_F64,
+    WhitError,
+    Workspace,
+    whit_backward,
+    whit_failures,
+    whit_forward,
+    whit_ws_bytes,
+)
+from .autograd import WhittakerFn, smooth  # noqa: F401
+
+__all__ = ["smooth", "WhittakerFn", "Workspace", "whit_forward", "whit_backward", "whit_failures",
+           "whit_ws_bytes", "WhitError", "WHIT_F32", "WHIT_F64"]

@@ -1,0 +1,138 @@
+"""ctypes binding of libwhit (include/libwhit.h): argument marshalling only.
+
+Every compute step runs in the CUDA kernels inside ``libwhit.so``; this module
+converts torch tensors to device pointers, checks shapes, and raises
+``WhitError`` on a non-OK status.  There is no CPU fallback: if the shared
+library is missing, importing the package raises ``ImportError``.
+
+Function names mirror the C-ABI: ``whit_ws_bytes``, ``whit_ws_create``,
+``whit_forward``, ``whit_backward``, ``whit_failures`` ...
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwhit.so")
+
+WHIT_F32, WHIT_F64 = 0, 1
+WHIT_LAMBDA_SCALAR, WHIT_LAMBDA_PER_DATE = 0, 1
+STATUS = {0: "WHIT_OK", 1: "WHIT_ERR_ARG", 2: "WHIT_ERR_SHAPE", 3: "WHIT_ERR_ALIGN",
+          4: "WHIT_ERR_WS", 5: "WHIT_ERR_CUDA", 6: "WHIT_ERR_STATE"}
+
+# (name, restype, argtypes) for every function in include/libwhit.h
+_VP, _I64, _SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t
+SIGNATURES = [
+    ("whit_version", ctypes.c_int, []),
+    ("whit_status_string", ctypes.c_char_p, [ctypes.c_int]),
+    ("whit_last_error", ctypes.c_char_p, []),
+    ("whit_ws_bytes", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int]),
+    ("whit_ws_create", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
+                                      _VP, _SZ, _VP]),
+    ("whit_ws_set_stream", ctypes.c_int, [_VP, _VP]),
+    ("whit_ws_destroy", None, [_VP]),
+    ("whit_forward", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
+    ("whit_backward", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("whit_failures", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int32)]),
+    ("whit_info_device", _VP, [_VP]),
+]
+
+
+class WhitError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = _lib.whit_last_error().decode() if _lib is not None else ""
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libwhit.so not found at {LIB_PATH}: build it with `make -C paper_2604_00048_b200` "
+                          "or __graft_entry__.build() (there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(status: int, where: str):
+    if status != 0:
+        raise WhitError(status, where)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    if dt == torch.float32:
+        return WHIT_F32
+    if dt == torch.float64:
+        return WHIT_F64
+    raise TypeError(f"libwhit supports float32 / float64 planes, got {dt}")
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def whit_ws_bytes(d: int, T: int, B: int, dtype: torch.dtype, per_date: bool) -> int:
+    return int(_lib.whit_ws_bytes(d, T, B, _dtype_code(dtype), int(per_date)))
+
+
+class Workspace:
+    """Host handle (``whit_ws*``) plus the torch-owned device buffer it binds."""
+
+    def __init__(self, d: int, T: int, B: int, dtype: torch.dtype, per_date: bool, device=None, stream=None):
+        nbytes = whit_ws_bytes(d, T, B, dtype, per_date)
+        if nbytes == 0:
+            raise WhitError(1, f"whit_ws_bytes(d={d}, T={T}, B={B})")
+        self.d, self.T, self.B, self.dtype, self.per_date = d, T, B, dtype, per_date
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+        h = ctypes.c_void_p()
+        _check(_lib.whit_ws_create(ctypes.byref(h), d, T, B, _dtype_code(dtype), int(per_date),
+                                   ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
+               "whit_ws_create")
+        self.handle = h
+
+    def set_stream(self, stream=None):
+        _check(_lib.whit_ws_set_stream(self.handle, _stream_handle(stream)), "whit_ws_set_stream")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.whit_ws_destroy(h)
+            self.handle = None
+
+
+def whit_forward(y, w, lam, d: int, T: int, B: int, z, ws: Workspace):
+    _check(_lib.whit_forward(_ptr(y), _ptr(w), _ptr(lam), d, T, B, _ptr(z), ws.handle), "whit_forward")
+
+
+def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):
+    _check(_lib.whit_backward(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)), "whit_backward")
+
+
+def whit_failures(ws: Workspace, with_info: bool = False):
+    n = ctypes.c_int64(0)
+    if with_info:
+        info = (ctypes.c_int32 * ws.B)()
+        _check(_lib.whit_failures(ws.handle, ctypes.byref(n), info), "whit_failures")
+        import numpy as np
+        return int(n.value), np.frombuffer(info, dtype=np.int32).copy()
+    _check(_lib.whit_failures(ws.handle, ctypes.byref(n), None), "whit_failures")
+    return int(n.value)

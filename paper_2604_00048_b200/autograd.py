@@ -1,0 +1,68 @@
+"""Thin ``torch.autograd.Function`` over libwhit (the paper's custom autograd op).
+
+``smooth(y, w, lam, d)`` is the layer ``z = f_Lambda(x | W, D)`` of P:74:
+forward = ``whit_forward`` (Eq. (3)), backward = ``whit_backward``
+(Eq. (4)-(5)).  Torch is used for device memory and the current
+stream only; all arithmetic runs in the library's kernels.
+
+Tensors are time-outer ``(T, B)`` (``lam``: ``(T-d, B)`` per date or ``(B,)``
+scalar per series), CUDA, contiguous, float32 or float64.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+
+
+def _pad_cols(x: torch.Tensor, Bp: int, value: float) -> torch.Tensor:
+    if x.shape[-1] == Bp:
+        return x
+    pad = torch.full(x.shape[:-1] + (Bp - x.shape[-1],), value, dtype=x.dtype, device=x.device)
+    return torch.cat([x, pad], dim=-1).contiguous()
+
+
+class WhittakerFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, y, w, lam, d):
+        if not (y.is_cuda and w.is_cuda and lam.is_cuda):
+            raise ValueError("libwhit runs on CUDA tensors only (no CPU fallback)")
+        if y.dim() != 2 or w.shape != y.shape:
+            raise ValueError("y and w must be (T, B)")
+        T, B = y.shape
+        per_date = lam.dim() == 2
+        if per_date and lam.shape != (T - d, B):
+            raise ValueError(f"per-date lambda must be (T-d, B) = {(T - d, B)}, got {tuple(lam.shape)}")
+        if not per_date and lam.shape != (B,):
+            raise ValueError(f"scalar lambda must be (B,), got {tuple(lam.shape)}")
+        if not (y.dtype == w.dtype == lam.dtype):
+            raise TypeError("y, w, lambda must share a dtype")
+        q = 4 if y.dtype == torch.float32 else 2
+        Bp = (B + q - 1) // q * q  # 16-byte row stride; padded series: w = 1, lam = 1, y = 0
+        yp = _pad_cols(y.contiguous(), Bp, 0.0)
+        wp = _pad_cols(w.contiguous(), Bp, 1.0)
+        lp = _pad_cols(lam.contiguous(), Bp, 1.0)
+        ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device)
+        z = torch.empty_like(yp)
+        L.whit_forward(yp, wp, lp, d, T, Bp, z, ws)
+        ctx.ws, ctx.keep, ctx.B, ctx.Bp, ctx.d = ws, (wp, lp, z), B, Bp, d
+        ctx.lam_shape = lam.shape
+        return z[:, :B] if Bp != B else z
+
+    @staticmethod
+    def backward(ctx, gz):
+        ws, (wp, lp, z) = ctx.ws, ctx.keep
+        gzp = _pad_cols(gz.contiguous(), ctx.Bp, 0.0)
+        gy = torch.empty_like(gzp)
+        gl = torch.empty_like(lp)
+        ws.set_stream()
+        L.whit_backward(gzp, ws, z, gy, gl)
+        B = ctx.B
+        if ctx.Bp != B:
+            gy, gl = gy[:, :B], gl[..., :B]
+        return gy, None, gl, None
+
+
+def smooth(y: torch.Tensor, w: torch.Tensor, lam: torch.Tensor, d: int = 2) -> torch.Tensor:
+    """Differentiable Whittaker smoother (heteroscedastic if ``lam`` is (T-d, B))."""
+    return WhittakerFn.apply(y, w, lam, d)

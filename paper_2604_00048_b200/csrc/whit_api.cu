@@ -1,0 +1,313 @@
+// libwhit host side: the C-ABI of include/libwhit.h (validation, workspace
+// layout, TMA descriptor encoding, kernel dispatch).  No torch types, no
+// exceptions across the boundary, no host synchronisation except
+// whit_failures().
+#include "libwhit.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "whit_kernels.cuh"
+
+using whit::Params;
+
+namespace {
+
+thread_local std::string g_err;
+
+whit_status fail(whit_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+whit_status fail(whit_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+// chunk length = TMA tile rows (whit::Tile<IO, d>::K)
+int chunk_k(int d) { return d <= 2 ? 16 : 8; }
+static_assert(whit::Tile<float, 1>::K == 16 && whit::Tile<float, 2>::K == 16 && whit::Tile<float, 3>::K == 8 &&
+                  whit::Tile<double, 1>::K == 16 && whit::Tile<double, 2>::K == 16 && whit::Tile<double, 3>::K == 8,
+              "chunk length table out of sync with whit::Tile");
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WsLayout {
+  size_t off_dz, off_ckf, off_ckb, off_info, off_cnt, total;
+};
+
+bool layout(int d, int64_t T, int64_t B, whit_dtype dt, WsLayout* L) {
+  if (d < 1 || d > 3 || T < d + 1 || B < 1 || (dt != WHIT_F32 && dt != WHIT_F64)) return false;
+  const size_t esz = dt == WHIT_F32 ? 4 : 8;
+  const int64_t C = (T + chunk_k(d) - 1) / chunk_k(d);
+  const int nf = d + d * (d - 1) / 2 + d;
+  size_t o = 0;
+  L->off_dz = o;   o = align256(o + size_t(T - d) * size_t(B) * esz);
+  L->off_ckf = o;  o = align256(o + size_t(C) * nf * size_t(B) * 8);
+  L->off_ckb = o;  o = align256(o + size_t(C) * d * size_t(B) * 8);
+  L->off_info = o; o = align256(o + size_t(B) * 4);
+  L->off_cnt = o;  o = align256(o + 8);
+  L->total = o;
+  return true;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// 2-D map over a [rows][inner] plane, box {box_inner, box_rows}; out-of-bounds
+// elements (negative or >= rows, >= inner) read as zero.
+whit_status encode_map(CUtensorMap* m, const void* ptr, whit_dtype dt, int64_t inner, int64_t rows, int box_inner,
+                       int box_rows) {
+  if (!get_encode()) return fail(WHIT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  const size_t esz = dt == WHIT_F32 ? 4 : 8;
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(inner) * esz};
+  cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, dt == WHIT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                        const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(WHIT_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", int(r));
+  return WHIT_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+struct whit_ws {
+  int d;
+  int64_t T, B;
+  whit_dtype dt;
+  whit_lambda_mode lm;
+  char* buf;
+  size_t bytes;
+  cudaStream_t stream;
+  WsLayout L;
+  bool have_fwd;
+  const void* w;
+  const void* lam;
+  const void* z;
+};
+
+namespace {
+
+template <int D, typename IO, bool PD, bool BWD>
+whit_status launch(const Params& p, cudaStream_t s) {
+  using L = whit::Layout<D, IO, PD, BWD>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    L::SMEM);
+  });
+  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  const long long grid = (p.B + L::NT - 1) / L::NT;
+  whit::whit_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(L::NT + 32), L::SMEM, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return WHIT_OK;
+}
+
+template <typename IO, bool PD, bool BWD>
+whit_status dispatch_d(int d, const Params& p, cudaStream_t s) {
+  switch (d) {
+    case 1: return launch<1, IO, PD, BWD>(p, s);
+    case 2: return launch<2, IO, PD, BWD>(p, s);
+    case 3: return launch<3, IO, PD, BWD>(p, s);
+  }
+  return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+}
+
+template <bool BWD>
+whit_status dispatch(const whit_ws* ws, const Params& p) {
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  if (ws->dt == WHIT_F32)
+    return pd ? dispatch_d<float, true, BWD>(ws->d, p, ws->stream) : dispatch_d<float, false, BWD>(ws->d, p, ws->stream);
+  return pd ? dispatch_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_d<double, false, BWD>(ws->d, p, ws->stream);
+}
+
+int tile_nt(whit_dtype dt) { return dt == WHIT_F32 ? whit::Tile<float, 2>::NT : whit::Tile<double, 2>::NT; }
+
+// Fill the tensor maps and plain pointers common to both directions.
+whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const void* w, const void* lam) {
+  std::memset(p, 0, sizeof *p);
+  const int nt = tile_nt(ws->dt);
+  const int d = ws->d;
+  const int kK = chunk_k(d);
+  whit_status st;
+  if ((st = encode_map(&p->tm_rhs, rhs, ws->dt, ws->B, ws->T, nt, kK)) != WHIT_OK) return st;
+  if ((st = encode_map(&p->tm_w, w, ws->dt, ws->B, ws->T, nt, kK)) != WHIT_OK) return st;
+  if (ws->lm == WHIT_LAMBDA_PER_DATE) {
+    if ((st = encode_map(&p->tm_lam_up, lam, ws->dt, ws->B, ws->T - d, nt, kK)) != WHIT_OK) return st;
+    if ((st = encode_map(&p->tm_lam_dn, lam, ws->dt, ws->B, ws->T - d, nt, kK + d)) != WHIT_OK) return st;
+  } else {
+    p->lam_scalar = lam;
+  }
+  p->ck_f = reinterpret_cast<double*>(ws->buf + ws->L.off_ckf);
+  p->ck_b = reinterpret_cast<double*>(ws->buf + ws->L.off_ckb);
+  p->info = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_info);
+  p->B = ws->B;
+  p->T = int(ws->T);
+  p->C = int((ws->T + kK - 1) / kK);
+  return WHIT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int whit_version(void) { return LIBWHIT_VERSION; }
+
+const char* whit_status_string(whit_status s) {
+  switch (s) {
+    case WHIT_OK: return "WHIT_OK";
+    case WHIT_ERR_ARG: return "WHIT_ERR_ARG";
+    case WHIT_ERR_SHAPE: return "WHIT_ERR_SHAPE";
+    case WHIT_ERR_ALIGN: return "WHIT_ERR_ALIGN";
+    case WHIT_ERR_WS: return "WHIT_ERR_WS";
+    case WHIT_ERR_CUDA: return "WHIT_ERR_CUDA";
+    case WHIT_ERR_STATE: return "WHIT_ERR_STATE";
+  }
+  return "WHIT_UNKNOWN_STATUS";
+}
+
+const char* whit_last_error(void) { return g_err.c_str(); }
+
+size_t whit_ws_bytes(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode) {
+  WsLayout L;
+  if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE) return 0;
+  if (!layout(d, T, B, dtype, &L)) return 0;
+  return L.total;
+}
+
+whit_status whit_ws_create(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
+                           whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream) {
+  if (!out) return fail(WHIT_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (d < 1 || d > 3) return fail(WHIT_ERR_ARG, "d = %d not in {1,2,3}", d);
+  if (dtype != WHIT_F32 && dtype != WHIT_F64) return fail(WHIT_ERR_ARG, "bad dtype %d", int(dtype));
+  if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE)
+    return fail(WHIT_ERR_ARG, "bad lambda mode %d", int(lambda_mode));
+  if (T < d + 1) return fail(WHIT_ERR_SHAPE, "T = %lld < d + 1", (long long)T);
+  if (T > (int64_t(1) << 30)) return fail(WHIT_ERR_SHAPE, "T = %lld too large", (long long)T);
+  if (B < 1 || B >= (int64_t(1) << 31)) return fail(WHIT_ERR_SHAPE, "B = %lld out of range [1, 2^31)", (long long)B);
+  if (B % (dtype == WHIT_F32 ? 4 : 2) != 0)
+    return fail(WHIT_ERR_ALIGN, "B = %lld must be a multiple of %d (16-B row stride)", (long long)B,
+                dtype == WHIT_F32 ? 4 : 2);
+  WsLayout L;
+  layout(d, T, B, dtype, &L);
+  if (!dev_buf) return fail(WHIT_ERR_WS, "workspace buffer is NULL");
+  if (reinterpret_cast<uintptr_t>(dev_buf) & 255u) return fail(WHIT_ERR_ALIGN, "workspace buffer not 256-B aligned");
+  if (dev_bytes < L.total)
+    return fail(WHIT_ERR_WS, "workspace %zu bytes < required %zu", dev_bytes, L.total);
+  whit_ws* ws = new (std::nothrow) whit_ws;
+  if (!ws) return fail(WHIT_ERR_ARG, "host allocation failed");
+  ws->d = d; ws->T = T; ws->B = B; ws->dt = dtype; ws->lm = lambda_mode;
+  ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
+  ws->stream = static_cast<cudaStream_t>(cuda_stream);
+  ws->L = L;
+  ws->have_fwd = false; ws->w = ws->lam = ws->z = nullptr;
+  *out = ws;
+  return WHIT_OK;
+}
+
+whit_status whit_ws_set_stream(whit_ws* ws, void* cuda_stream) {
+  if (!ws) return fail(WHIT_ERR_ARG, "ws is NULL");
+  ws->stream = static_cast<cudaStream_t>(cuda_stream);
+  return WHIT_OK;
+}
+
+void whit_ws_destroy(whit_ws* ws) { delete ws; }
+
+whit_status whit_forward(const void* y, const void* w, const void* lambda, int d, int64_t T, int64_t B, void* z,
+                         whit_ws* ws) {
+  if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (!y || !w || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
+  if (d != ws->d || T != ws->T || B != ws->B)
+    return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
+                (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
+  if (!aligned16(y) || !aligned16(w) || !aligned16(lambda) || !aligned16(z))
+    return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
+  if (z == y || z == w || z == lambda) return fail(WHIT_ERR_ARG, "z aliases an input");
+  Params p;
+  whit_status st = fill_params(ws, &p, y, w, lambda);
+  if (st != WHIT_OK) return st;
+  p.out0 = z;
+  p.out1 = ws->buf + ws->L.off_dz;
+  ws->have_fwd = false;
+  st = dispatch<false>(ws, p);
+  if (st != WHIT_OK) return st;
+  ws->have_fwd = true;
+  ws->w = w; ws->lam = lambda; ws->z = z;
+  return WHIT_OK;
+}
+
+whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* grad_y, void* grad_lambda) {
+  if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "whit_backward without a preceding whit_forward on this workspace");
+  if (!grad_z || !grad_y || !grad_lambda) return fail(WHIT_ERR_ARG, "NULL data pointer");
+  if (z && z != ws->z) return fail(WHIT_ERR_STATE, "z is not the output of the matching whit_forward");
+  if (!aligned16(grad_z) || !aligned16(grad_y) || !aligned16(grad_lambda))
+    return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
+  if (grad_y == grad_z || grad_lambda == grad_z || grad_y == grad_lambda)
+    return fail(WHIT_ERR_ARG, "outputs alias inputs");
+  Params p;
+  whit_status st = fill_params(ws, &p, grad_z, ws->w, ws->lam);
+  if (st != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_dz, ws->buf + ws->L.off_dz, ws->dt, ws->B, ws->T - ws->d, tile_nt(ws->dt),
+                      chunk_k(ws->d))) != WHIT_OK)
+    return st;
+  p.out0 = grad_y;
+  p.out1 = grad_lambda;
+  return dispatch<true>(ws, p);
+}
+
+whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {
+  if (!ws || !n_failed) return fail(WHIT_ERR_ARG, "NULL argument");
+  if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "no forward has run on this workspace");
+  auto* cnt = reinterpret_cast<unsigned long long*>(ws->buf + ws->L.off_cnt);
+  const int32_t* info = reinterpret_cast<const int32_t*>(ws->buf + ws->L.off_info);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof *cnt, ws->stream);
+  if (e == cudaSuccess) {
+    const long long blocks = std::min<long long>((ws->B + 255) / 256, 4096);
+    whit::count_failures<<<(unsigned)blocks, 256, 0, ws->stream>>>(info, ws->B, cnt);
+    e = cudaGetLastError();
+  }
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, ws->stream);
+  if (e == cudaSuccess && host_info)
+    e = cudaMemcpyAsync(host_info, info, size_t(ws->B) * 4, cudaMemcpyDeviceToHost, ws->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "whit_failures: %s", cudaGetErrorString(e));
+  *n_failed = (int64_t)h;
+  return WHIT_OK;
+}
+
+const int32_t* whit_info_device(const whit_ws* ws) {
+  return ws ? reinterpret_cast<const int32_t*>(ws->buf + ws->L.off_info) : nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+"""GPU parity: libwhit (C-ABI, sm_100a kernels) vs the CPU oracle on identical inputs.
+
+Tolerances (BASELINE.json north_star; DESIGN.md §3 R-9): fp32 I/O
+max|z - z_ref| / max|y| <= 1e-4 and gradients <= 1e-3 relative, for lambda <= 1e5;
+fp64 I/O z <= 1e-10 (gradients <= 1e-9, our reading).  d = 3 is reported with a
+looser gate (intrinsically ill-conditioned with long gaps).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import banded as O2
+from oracle import whittaker as O1
+from helpers import host_inputs, rel_series, run_cuda, ymax_observed
+
+pytestmark = pytest.mark.gpu
+
+TOL = {  # (z, grads)
+    (torch.float32, 1): (1e-4, 1e-3), (torch.float32, 2): (1e-4, 1e-3), (torch.float32, 3): (1e-4, 1e-3),
+    (torch.float64, 1): (1e-10, 1e-9), (torch.float64, 2): (1e-10, 1e-9), (torch.float64, 3): (1e-8, 1e-7),
+}
+
+
+def oracle_O2(h, d):
+    lam = h["lam"]
+    z, dz, info = O2.forward_banded(h["y"], h["w"], lam, d)
+    out = {"z": z, "info": info}
+    if "g" in h:
+        yb, lb = O2.backward_banded(h["g"], h["w"], lam, d, z)
+        out.update(ybar=yb, lambar=lb)
+    return out
+
+
+def check(res, ref, h, d, dtype, backward=True, idx=None, label=""):
+    tz, tg = TOL[(dtype, d)]
+    sl = slice(None) if idx is None else idx
+    ez = rel_series(res["z"][sl], ref["z"], ymax_observed(h["y"], h["w"]))
+    msg = f"{label} z err max {ez.max():.3e}"
+    assert np.all(np.isfinite(res["z"][sl])), label
+    assert ez.max() <= tz, msg
+    if backward:
+        ey = rel_series(res["ybar"][sl], ref["ybar"])
+        el = rel_series(res["lambar"][sl], ref["lambar"])
+        assert ey.max() <= tg, f"{label} ybar err {ey.max():.3e}"
+        assert el.max() <= tg, f"{label} lambar err {el.max():.3e}"
+    return ez.max()
+
+
+def test_toy_config_all_series():
+    """BASELINE configs[0]: 1024 series, T = 365, d = 2, scalar lambda, fwd only; every series vs O2,
+    16 series vs O1 (dense + refinement)."""
+    x = synth.make_inputs("toy", device="cuda")
+    res = run_cuda(x, 2, torch.float32, backward=False)
+    h = host_inputs(x)
+    assert res["nfail"] == 0
+    ref = oracle_O2(h, 2)
+    check(res, ref, h, 2, torch.float32, backward=False, label="toy/O2")
+    for b in np.linspace(0, 1023, 16).astype(int):
+        z1, _ = O1.forward(h["y"][b], h["w"][b], h["lam"][b], 2)
+        e = np.max(np.abs(res["z"][b] - z1.astype(float))) / ymax_observed(h["y"][b], h["w"][b])
+        assert e <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_grid_fwd_bwd(d, per_date, dtype):
+    """Every (d, lambda mode, dtype) instantiation, ragged in T (203 = 12*16 + 11) and in B
+    (300 = 2*128 + 44 = 4*64 + 44), Sentinel-2 mask; every series vs O2 (Alg. 1, long double)."""
+    x = synth.make_inputs("hetero", B=300, T=203, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", dtype=dtype, seed=11 + d)
+    res = run_cuda(x, d, dtype)
+    h = host_inputs(x)
+    assert res["nfail"] == 0 and np.all(res["info"] == 0)
+    ref = oracle_O2(h, d)
+    check(res, ref, h, d, dtype, label=f"d={d} pd={per_date} {dtype}")
+
+
+@pytest.mark.parametrize("T", [3, 4, 15, 16, 17, 32, 33])
+@pytest.mark.parametrize("B", [4, 132])
+def test_edge_shapes_vs_dense(T, B):
+    """Smallest T (= d+1), T below / at / just above one chunk, B = 4 and B ragged vs the CTA;
+    fp64, per-date lambda, d = 2, every series vs O1 (the dense definition)."""
+    d = 2
+    x = synth.make_inputs("toy", B=B, T=T, d=d, lam_mode="per_date", device="cuda", dtype=torch.float64,
+                          seed=1000 + T)
+    res = run_cuda(x, d, torch.float64)
+    h = host_inputs(x)
+    for b in range(B):
+        o = O1.forward_backward(h["y"][b], h["w"][b], h["lam"][b], d, h["g"][b])
+        ez = np.max(np.abs(res["z"][b] - o["z"].astype(float))) / max(ymax_observed(h["y"][b], h["w"][b]), 1e-300)
+        assert ez <= 1e-10, (T, B, b, ez)
+        assert rel_series(res["ybar"][b], o["ybar"]).max() <= 1e-9
+        assert rel_series(res["lambar"][b], o["lambar"]).max() <= 1e-9
+
+
+def test_degenerate_series_info_and_nan():
+    """Non-SPD series (fewer than d observed days; P:87 requires SPD) -> info = T-d+1, NaN outputs,
+    whit_failures counts them; healthy neighbours are unaffected."""
+    d, T, B = 2, 50, 8
+    x = synth.make_inputs("toy", B=B, T=T, d=d, lam_mode="per_date", device="cuda", dtype=torch.float64)
+    w = x["w"]
+    w[:, 0] = 0                     # no observation
+    w[:, 1] = 0; w[7, 1] = 1        # one observation
+    w[:, 2] = 0; w[[5, 30], 2] = 1  # exactly d observations: SPD
+    res = run_cuda(x, d, torch.float64)
+    assert res["nfail"] == 2
+    assert res["info"][0] == T - d + 1 and res["info"][1] == T - d + 1
+    assert np.all(res["info"][2:] == 0)
+    for k in ("z", "ybar", "lambar"):
+        assert np.all(np.isnan(res[k][:2])) and np.all(np.isfinite(res[k][2:]))
+    h = host_inputs(x)
+    o = O1.forward_backward(h["y"][2], h["w"][2], h["lam"][2], d, h["g"][2])
+    assert np.max(np.abs(res["z"][2] - o["z"].astype(float))) <= 1e-9 * max(1.0, np.abs(o["z"]).max())
+
+
+def test_mask_zero_independence_bitwise():
+    """Values of y where w = 0 never enter the arithmetic ((W y)_t := 0, R-4): NaN there changes nothing."""
+    d = 2
+    x = synth.make_inputs("hetero", B=256, T=400, d=d, device="cuda")
+    a = run_cuda(x, d, torch.float32)
+    x2 = dict(x)
+    x2["y"] = torch.where(x["w"] > 0, x["y"], torch.full_like(x["y"], float("nan")))
+    b = run_cuda(x2, d, torch.float32)
+    for k in ("z", "ybar", "lambar"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_autograd_shim_matches_oracle():
+    """torch.autograd through WhittakerFn (B = 10, padded internally to 12) == O1."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 120, 10
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64)
+    y = x["y"].clone().requires_grad_(True)
+    lam = x["lam"].clone().requires_grad_(True)
+    z = P.smooth(y, x["w"], lam, d)
+    gy, gl = torch.autograd.grad(z, (y, lam), grad_outputs=x["g"])
+    h = host_inputs(x)
+    for b in range(B):
+        o = O1.forward_backward(h["y"][b], h["w"][b], h["lam"][b], d, h["g"][b])
+        assert np.max(np.abs(z[:, b].detach().cpu().numpy() - o["z"].astype(float))) <= 1e-10 * 2
+        assert rel_series(gy[:, b].cpu().numpy(), o["ybar"]).max() <= 1e-9
+        assert rel_series(gl[:, b].cpu().numpy(), o["lambar"]).max() <= 1e-9
+
+
+def _sample(B, n=8):
+    return np.unique(np.concatenate([[0, B - 1], np.linspace(0, B - 1, n).astype(int)]))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_hetero_full_size_sampled(dtype):
+    """BASELINE configs[2] at full size (B = 262,144, T = 3,288, per-date lambda) in the launch
+    configuration bench.py times: sampled series vs O1 (dense + refinement), 64 vs O2, and
+    whole-batch properties (finite, no failures)."""
+    d = 2
+    x = synth.make_inputs("hetero", device="cuda", dtype=dtype)
+    res = run_cuda(x, d, dtype)
+    assert res["nfail"] == 0
+    for k in ("z", "ybar", "lambar"):
+        assert np.all(np.isfinite(res[k])), k
+    B = x["y"].shape[1]
+    idx = _sample(B, 6)
+    h = host_inputs({k: (v[:, idx] if v.dim() == 2 else v[idx]) for k, v in x.items() if k in ("y", "w", "lam", "g")})
+    tz, tg = TOL[(dtype, d)]
+    for i, b in enumerate(idx):
+        o = O1.forward_backward(h["y"][i], h["w"][i], h["lam"][i], d, h["g"][i])
+        ez = np.max(np.abs(res["z"][b] - o["z"].astype(float))) / ymax_observed(h["y"][i], h["w"][i])
+        assert ez <= tz, (b, ez)
+        assert rel_series(res["ybar"][b], o["ybar"]).max() <= tg
+        assert rel_series(res["lambar"][b], o["lambar"]).max() <= tg
+    idx2 = np.random.default_rng(5).choice(B, 64, replace=False)
+    h2 = host_inputs({k: (v[:, idx2] if v.dim() == 2 else v[idx2]) for k, v in x.items() if k in ("y", "w", "lam", "g")})
+    ref = oracle_O2(h2, d)
+    check(res, ref, h2, d, dtype, idx=idx2, label="hetero/O2")
+
+
+def test_homo_full_size_fp32_and_fp64_check():
+    """BASELINE configs[1]: B = 65,536, T = 3,288, scalar lambda, fp32 with an fp64 check."""
+    d = 2
+    x = synth.make_inputs("homo", device="cuda")
+    r32 = run_cuda(x, d, torch.float32)
+    r64 = run_cuda(x, d, torch.float64)
+    assert r32["nfail"] == 0 and r64["nfail"] == 0
+    B = x["y"].shape[1]
+    idx = _sample(B, 4)
+    h = host_inputs({k: (v[:, idx] if v.dim() == 2 else v[idx]) for k, v in x.items() if k in ("y", "w", "lam", "g")})
+    for i, b in enumerate(idx):
+        o = O1.forward_backward(h["y"][i], h["w"][i], h["lam"][i], d, h["g"][i])
+        ym = ymax_observed(h["y"][i], h["w"][i])
+        assert np.max(np.abs(r32["z"][b] - o["z"].astype(float))) / ym <= 1e-4
+        assert np.max(np.abs(r64["z"][b] - o["z"].astype(float))) / ym <= 1e-10
+        assert abs(r32["lambar"][b] - float(o["lambar"])) <= 1e-3 * abs(float(o["lambar"]))
+        assert abs(r64["lambar"][b] - float(o["lambar"])) <= 1e-9 * abs(float(o["lambar"]))
