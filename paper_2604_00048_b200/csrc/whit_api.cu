@@ -36,8 +36,8 @@ whit_status fail(whit_status s, const char* fmt, ...) {
 
 // chunk length = TMA tile rows (whit::Tile<IO, d>::K)
 int chunk_k(int d) { return d <= 2 ? 16 : 8; }
-static_assert(whit::Tile<float, 1>::K == 16 && whit::Tile<float, 2>::K == 16 && whit::Tile<float, 3>::K == 8 &&
-                  whit::Tile<double, 1>::K == 16 && whit::Tile<double, 2>::K == 16 && whit::Tile<double, 3>::K == 8,
+static_assert(whit::Tile<float, 1, false>::K == 16 && whit::Tile<float, 2, true>::K == 16 && whit::Tile<float, 3, false>::K == 8 &&
+                  whit::Tile<double, 1, true>::K == 16 && whit::Tile<double, 2, false>::K == 16 && whit::Tile<double, 3, true>::K == 8,
               "chunk length table out of sync with whit::Tile");
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -98,6 +98,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 }  // namespace
 
 struct whit_ws {
+  int device;  // CUDA device current at creation (-1: none), made current around encodes/launches
   int d;
   int64_t T, B;
   whit_dtype dt;
@@ -114,6 +115,22 @@ struct whit_ws {
 
 namespace {
 
+// Makes the workspace's device current on the calling thread (autograd runs
+// backward on its own device thread, where no context is bound yet) and
+// restores the caller's device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (dev < 0) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <int D, typename IO, bool PD, bool BWD>
 whit_status launch(const Params& p, cudaStream_t s) {
   using L = whit::Layout<D, IO, PD, BWD>;
@@ -124,8 +141,9 @@ whit_status launch(const Params& p, cudaStream_t s) {
                                     L::SMEM);
   });
   if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  const long long grid = (p.B + L::NT - 1) / L::NT;
-  whit::whit_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(L::NT + 32), L::SMEM, s>>>(p);
+  constexpr int per_cta = 32 * L::WARPS;  // one series per thread, one TMA pipeline per warp
+  const long long grid = (p.B + per_cta - 1) / per_cta;
+  whit::whit_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(per_cta), L::SMEM, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
@@ -149,7 +167,8 @@ whit_status dispatch(const whit_ws* ws, const Params& p) {
   return pd ? dispatch_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_d<double, false, BWD>(ws->d, p, ws->stream);
 }
 
-int tile_nt(whit_dtype dt) { return dt == WHIT_F32 ? whit::Tile<float, 2>::NT : whit::Tile<double, 2>::NT; }
+// TMA box inner extent: one warp's 32 series.
+int tile_nt(whit_dtype) { return 32; }
 
 // Fill the tensor maps and plain pointers common to both directions.
 whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const void* w, const void* lam) {
@@ -163,6 +182,7 @@ whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const voi
   if (ws->lm == WHIT_LAMBDA_PER_DATE) {
     if ((st = encode_map(&p->tm_lam_up, lam, ws->dt, ws->B, ws->T - d, nt, kK)) != WHIT_OK) return st;
     if ((st = encode_map(&p->tm_lam_dn, lam, ws->dt, ws->B, ws->T - d, nt, kK + d)) != WHIT_OK) return st;
+    p->lam_plane = lam;
   } else {
     p->lam_scalar = lam;
   }
@@ -230,6 +250,10 @@ whit_status whit_ws_create(whit_ws** out, int d, int64_t T, int64_t B, whit_dtyp
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
   ws->have_fwd = false; ws->w = ws->lam = ws->z = nullptr;
+  ws->device = -1;
+  int dev = -1;
+  if (cudaGetDevice(&dev) == cudaSuccess) ws->device = dev;
+  cudaGetLastError();  // creation is host-only: a missing GPU is not an error here
   *out = ws;
   return WHIT_OK;
 }
@@ -252,11 +276,16 @@ whit_status whit_forward(const void* y, const void* w, const void* lambda, int d
   if (!aligned16(y) || !aligned16(w) || !aligned16(lambda) || !aligned16(z))
     return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
   if (z == y || z == w || z == lambda) return fail(WHIT_ERR_ARG, "z aliases an input");
+  DeviceGuard guard(ws->device);
+  if (!guard.ok) return fail(WHIT_ERR_CUDA, "cudaSetDevice(%d) failed", ws->device);
   Params p;
   whit_status st = fill_params(ws, &p, y, w, lambda);
   if (st != WHIT_OK) return st;
   p.out0 = z;
   p.out1 = ws->buf + ws->L.off_dz;
+  const int kK = chunk_k(d);
+  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, tile_nt(ws->dt), kK)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out1, p.out1, ws->dt, B, T - d, tile_nt(ws->dt), kK)) != WHIT_OK) return st;
   ws->have_fwd = false;
   st = dispatch<false>(ws, p);
   if (st != WHIT_OK) return st;
@@ -274,6 +303,8 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
     return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
   if (grad_y == grad_z || grad_lambda == grad_z || grad_y == grad_lambda)
     return fail(WHIT_ERR_ARG, "outputs alias inputs");
+  DeviceGuard guard(ws->device);
+  if (!guard.ok) return fail(WHIT_ERR_CUDA, "cudaSetDevice(%d) failed", ws->device);
   Params p;
   whit_status st = fill_params(ws, &p, grad_z, ws->w, ws->lam);
   if (st != WHIT_OK) return st;
@@ -282,12 +313,18 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
     return st;
   p.out0 = grad_y;
   p.out1 = grad_lambda;
+  const int kK = chunk_k(ws->d);
+  if ((st = encode_map(&p.tm_out0, grad_y, ws->dt, ws->B, ws->T, tile_nt(ws->dt), kK)) != WHIT_OK) return st;
+  if (ws->lm == WHIT_LAMBDA_PER_DATE &&
+      (st = encode_map(&p.tm_out1, grad_lambda, ws->dt, ws->B, ws->T - ws->d, tile_nt(ws->dt), kK)) != WHIT_OK)
+    return st;
   return dispatch<true>(ws, p);
 }
 
 whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {
   if (!ws || !n_failed) return fail(WHIT_ERR_ARG, "NULL argument");
   if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "no forward has run on this workspace");
+  DeviceGuard guard(ws->device);
   auto* cnt = reinterpret_cast<unsigned long long*>(ws->buf + ws->L.off_cnt);
   const int32_t* info = reinterpret_cast<const int32_t*>(ws->buf + ws->L.off_info);
   cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof *cnt, ws->stream);

@@ -3,9 +3,10 @@
 // and its adjoint (Eq. (4)-(5)), one series per thread, fp64 math.
 //
 // Design:
-//  * layout [T][B]: one time row of a CTA's NT series is NT contiguous
-//    elements; a TMA 2-D box {NT series x K steps} stages a time tile of each
-//    input plane into a shared-memory ring fed by one producer warp;
+//  * layout [T][B]: one time row of a warp's 32 series is 32 contiguous
+//    elements; each warp runs its own TMA pipeline: lane 0 stages 2-D boxes
+//    {32 series x K steps} of every input plane into a private shared-memory
+//    ring (mbarrier complete_tx), so warps never wait on each other;
 //  * the band row of Omega is never materialised: it is assembled in
 //    registers from w_t, lambda_{t-d..t} and the constant stencil;
 //  * banded LDL^T in "deviation form" (R-10): L = M + A,
@@ -44,12 +45,15 @@ __host__ __device__ __forceinline__ constexpr double Cj(int d, int j) {
 
 // ------------------------------------------------------------------ kernel parameters
 struct Params {
-  CUtensorMap tm_rhs;     // y (forward) or grad_z (backward): [T][B], box {NT, K}
-  CUtensorMap tm_w;       // w: [T][B], box {NT, K}
-  CUtensorMap tm_lam_up;  // per-date lambda [T-d][B], box {NT, K}
-  CUtensorMap tm_lam_dn;  // per-date lambda [T-d][B], box {NT, K+d} (rows t0-d..t0+K-1)
-  CUtensorMap tm_dz;      // D z cache [T-d][B], box {NT, K} (backward only)
+  CUtensorMap tm_rhs;     // y (forward) or grad_z (backward): [T][B], box {32, K}
+  CUtensorMap tm_w;       // w: [T][B], box {32, K}
+  CUtensorMap tm_lam_up;  // per-date lambda [T-d][B], box {32, K}
+  CUtensorMap tm_lam_dn;  // per-date lambda [T-d][B], box {32, K+d} (rows t0-d..t0+K-1)
+  CUtensorMap tm_dz;      // D z cache [T-d][B], box {32, K} (backward only)
+  CUtensorMap tm_out0;    // z (forward) / grad_y (backward): [T][B], box {32, K}  (TMA store)
+  CUtensorMap tm_out1;    // D z (forward) / per-date grad_lambda (backward): [T-d][B], box {32, K}
   const void* lam_scalar; // [B] (scalar lambda mode)
+  const void* lam_plane;  // [T-d][B] (per-date mode; read directly only by the cold failure path)
   void* out0;             // forward: z [T][B]; backward: grad_y [T][B]
   void* out1;             // forward: D z [T-d][B] (ws); backward: grad_lambda
   double* ck_f;           // forward checkpoints [C][NF][B]  (factor + rhs state)
@@ -70,9 +74,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -97,8 +98,21 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until the TMA engine has finished READING the smem of all committed stores.
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// Wait until all committed stores are complete (globally visible).
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Order this warp's earlier generic-proxy reads of a stage before the TMA
+// (async proxy) write that refills it.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // fp64 reciprocal: MUFU.RCP64H seed + 2 Newton steps (error ~1 ulp).  Used
@@ -113,8 +127,19 @@ __device__ __forceinline__ double rcp64(double x) {
   return r;
 }
 
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000LL); }
+
 template <typename IO> __device__ __forceinline__ double to_f64(IO v) { return static_cast<double>(v); }
 template <typename IO> __device__ __forceinline__ IO from_f64(double v) { return static_cast<IO>(v); }
+
+// Right-hand side of the row: forward b_t = (W y)_t with (W y)_t := 0 where
+// w_t = 0 (R-4: values at masked slots, NaN included, never enter), selected
+// on the raw I/O value before widening; backward b_t = g_t.
+template <typename IO, bool BWD>
+__device__ __forceinline__ double rhs_times_w(IO rhs, IO wio, double w) {
+  if (BWD) return to_f64<IO>(rhs);
+  return w * to_f64<IO>(wio != IO(0) ? rhs : IO(0));
+}
 
 // ------------------------------------------------------------------ recurrence state
 // State entering row t: values of rows t-1..t-D (index i <-> row t-1-i).
@@ -138,34 +163,40 @@ template <int D> __device__ __forceinline__ void state_init(FState<D>& s) {
 
 // One row t of the deviation-form banded LDL^T fused with forward
 // substitution.  Recurrences (DESIGN.md §3 R-10, derived there):
-//   E_m  = -sum_{j=m+1..D} ( M_j lam~[t-j] A[t-m][j-m] + E_j (M_{j-m} + A[t-m][j-m]) ),  m = D..1
+//   E_D  = 0
+//   E_m  = -sum_{j=m+1..D} ( M_j lam~[t-j] A[t-m][j-m] + E_j (M_{j-m} + A[t-m][j-m]) ),  m = D-1..1
 //   A_m  = ( E_m - M_m Delta[t-m] ) / D[t-m]                 (L[t][t-m] = M_m + A_m)
 //   Delta_t = w_t - sum_j ( M_j E_j + A_j (M_j lam~[t-j] + E_j) )
 //   D_t  = lam~_t + Delta_t                                   (SPD <=> D_t > 0 for all t)
 //   v_t  = b_t - sum_j M_j v[t-j] - sum_j A_j v[t-j]
 // Outputs A[0..D-1] (= A_{t,1..D}), D_t, 1/D_t, v_t; advances the state.
+// Terms with E_D = 0 are dropped at compile time (an fma with a zero operand
+// is not foldable under IEEE rules, so it must not be written).
 template <int D>
 __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, double b, double (&A)[D],
                                          double& Dt, double& idt, double& vt) {
   double E[D + 1];
+  E[D] = 0.0;
+  A[D - 1] = (-Mj(D, D) * s.dl[D - 1]) * s.id[D - 1];
 #pragma unroll
-  for (int m = D; m >= 1; --m) {
-    double e = 0.0;
+  for (int m = D - 1; m >= 1; --m) {
+    // j = D term (E_D = 0): - M_D lam~[t-D] A[t-m][D-m]
+    double e = (-(Mj(D, D) * s.lm[D - 1])) * s.ap[m - 1][D - m - 1];
 #pragma unroll
-    for (int j = m + 1; j <= D; ++j) {
+    for (int j = D - 1; j >= m + 1; --j) {
       const double a = s.ap[m - 1][j - m - 1];
       e = fma(-(Mj(D, j) * s.lm[j - 1]), a, e);
       e = fma(-E[j], a, e);
       e = fma(-Mj(D, j - m), E[j], e);
     }
     E[m] = e;
-    const double num = (m == D) ? (-Mj(D, m) * s.dl[m - 1]) : fma(-Mj(D, m), s.dl[m - 1], e);
-    A[m - 1] = num * s.id[m - 1];
+    A[m - 1] = fma(-Mj(D, m), s.dl[m - 1], e) * s.id[m - 1];
   }
   double dl = w;
 #pragma unroll
+  for (int j = 1; j < D; ++j) dl = fma(-Mj(D, j), E[j], dl);
+#pragma unroll
   for (int j = 1; j <= D; ++j) {
-    if (j < D) dl = fma(-Mj(D, j), E[j], dl);
     const double inner = (j < D) ? fma(Mj(D, j), s.lm[j - 1], E[j]) : Mj(D, j) * s.lm[j - 1];
     dl = fma(-A[j - 1], inner, dl);
   }
@@ -197,107 +228,242 @@ template <int D> struct Ck {
 };
 
 // ------------------------------------------------------------------ tiling config
-// NT series per CTA (one per consumer thread), K time steps per chunk/tile,
-// ST ring stages.  K = 16 for d <= 2; d = 3 keeps 4 fp64 values per chunk row
-// in registers, so its chunk is 8 steps.  MAXREG keeps 2 CTAs (10 warps)/SM.
-template <typename IO, int D> struct Tile {
-  static constexpr int NT = sizeof(IO) == 4 ? 128 : 64;
+// One warp = 32 series = one TMA pipeline.  K time steps per chunk/tile, ST
+// ring stages per warp, WARPS warps per CTA.  K = 16 for d <= 2; d = 3 keeps
+// 4 fp64 values per chunk row in registers, so its chunk is 8 steps.
+// Registers are allocated per pair of warps, so CTAs are 4 warps; the forward
+// runs 3 CTAs (12 warps, <= 168 regs) per SM, the backward (one more staged
+// input plane) 2 CTAs (8 warps, <= 255 regs) so its rings fit in 227 KB.
+template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int K = D <= 2 ? 16 : 8;
-  static constexpr int ST = 3;
-  static constexpr int MAXREG = sizeof(IO) == 4 ? 200 : 255;
+  static constexpr int ST = 2;
+  static constexpr int WARPS = 4;
+  static constexpr int MAXREG = (BWD || sizeof(IO) == 8) ? 255 : 168;
 };
 
 template <int D, typename IO, bool PD, bool BWD> struct Layout {
-  static constexpr int NT = Tile<IO, D>::NT, K = Tile<IO, D>::K, ST = Tile<IO, D>::ST;
-  static constexpr int ROW = NT * (int)sizeof(IO);  // bytes of one staged time row
+  static constexpr int K = Tile<IO, D, BWD>::K, ST = Tile<IO, D, BWD>::ST, WARPS = Tile<IO, D, BWD>::WARPS;
+  static constexpr int ROW = 32 * (int)sizeof(IO);  // bytes of one staged time row (one warp)
   static constexpr int OFF_RHS = 0;
   static constexpr int OFF_W = K * ROW;
   static constexpr int OFF_LAM = 2 * K * ROW;
   static constexpr int OFF_DZ = OFF_LAM + (PD ? (K + D) * ROW : 0);
-  static constexpr int STAGE = OFF_DZ + (BWD ? K * ROW : 0);
-  static constexpr int SMEM = ST * STAGE;
+  static constexpr int STAGE = (OFF_DZ + (BWD ? K * ROW : 0) + 127) / 128 * 128;
+  static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
+  static constexpr int WARP_SMEM = ST * STAGE + 2 * OUT;     // ring + out0 + out1
+  static constexpr int SMEM = WARPS * WARP_SMEM;
   static constexpr uint32_t BYTES_UP = (2 * K + (PD ? K : 0)) * ROW;
   static constexpr uint32_t BYTES_DN = (2 * K + (PD ? K + D : 0) + (BWD ? K : 0)) * ROW;
 };
 
-// ------------------------------------------------------------------ the kernel
-// One launch = one full forward (BWD=false) or backward (BWD=true) for NT
-// series per CTA: up sweep over C chunks, then down sweep over C chunks.
+// Issue tile i (up sweep tiles 0..C-1, then down sweep C-1..0) of one warp.
 template <int D, typename IO, bool PD, bool BWD>
-__global__ void __maxnreg__((Tile<IO, D>::MAXREG)) whit_kernel(const __grid_constant__ Params p) {
+__device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage, uint64_t* bar, int i, int C,
+                                           int c0) {
   using L = Layout<D, IO, PD, BWD>;
-  constexpr int NT = L::NT, K = L::K, ST = L::ST;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[ST];
-  __shared__ __align__(8) uint64_t empty_bar[ST];
-
-  const int tid = threadIdx.x;
-  const int T = p.T, C = p.C;
-  const long long B = p.B;
-  const long long b0 = (long long)blockIdx.x * NT;
-
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], NT / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const bool up = i < C;
+  const int c = up ? i : 2 * C - 1 - i;
+  const int t0 = c * L::K;
+  mbar_arrive_expect_tx(bar, up ? L::BYTES_UP : L::BYTES_DN);
+  tma_load_2d(stage + L::OFF_RHS, &p.tm_rhs, c0, t0, bar);
+  tma_load_2d(stage + L::OFF_W, &p.tm_w, c0, t0, bar);
+  if (PD) {
+    if (up) tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_up, c0, t0, bar);
+    else tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_dn, c0, t0 - D, bar);
   }
-  __syncthreads();
+  if (BWD && !up) tma_load_2d(stage + L::OFF_DZ, &p.tm_dz, c0, t0, bar);
+}
 
-  // ---------------------------------------------------------------- producer warp
-  if (tid >= NT) {
-    if (tid == NT) {
-      prefetch_map(&p.tm_rhs);
-      prefetch_map(&p.tm_w);
-      if (PD) { prefetch_map(&p.tm_lam_up); prefetch_map(&p.tm_lam_dn); }
-      if (BWD) prefetch_map(&p.tm_dz);
-      for (int i = 0; i < 2 * C; ++i) {
-        const int s = i % ST;
-        const uint32_t ph = (uint32_t)((i / ST) & 1);
-        mbar_wait(&empty_bar[s], ph ^ 1u);
-        const bool up = i < C;
-        const int c = up ? i : 2 * C - 1 - i;
-        const int t0 = c * K;
-        unsigned char* st = smem + s * L::STAGE;
-        mbar_arrive_expect_tx(&full_bar[s], up ? L::BYTES_UP : L::BYTES_DN);
-        tma_load_2d(st + L::OFF_RHS, &p.tm_rhs, (int)b0, t0, &full_bar[s]);
-        tma_load_2d(st + L::OFF_W, &p.tm_w, (int)b0, t0, &full_bar[s]);
-        if (PD) {
-          if (up) tma_load_2d(st + L::OFF_LAM, &p.tm_lam_up, (int)b0, t0, &full_bar[s]);
-          else tma_load_2d(st + L::OFF_LAM, &p.tm_lam_dn, (int)b0, t0 - D, &full_bar[s]);
-        }
-        if (BWD && !up) tma_load_2d(st + L::OFF_DZ, &p.tm_dz, (int)b0, t0, &full_bar[s]);
+// ------------------------------------------------------------------ per-thread sweep bodies
+template <int D, typename IO, bool PD, bool BWD>
+struct Sweep {
+  using L = Layout<D, IO, PD, BWD>;
+  static constexpr int K = L::K;
+
+  // ---- up sweep over one chunk (rows t0..t0+K-1); RAGGED: the chunk reaches row T-D or beyond
+  template <bool RAGGED>
+  static __device__ __forceinline__ void up_chunk(FState<D>& st, const unsigned char* stg, int lane, int t0, int T,
+                                                  double lam_s, int& nobs, bool& pos) {
+    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;
+    const int TmD = T - D;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int t = t0 + k;
+      if (RAGGED && t >= T) break;  // rows past the end: nothing uses the state after row T-1
+      const IO wio = t_w[k * 32];
+      const double w = to_f64<IO>(wio);
+      double lt = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
+      if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
+      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+      double A[D], Dt, idt, vt;
+      ldl_step<D>(st, w, lt, bb, A, Dt, idt, vt);
+      if (!BWD) {
+        nobs += (wio > IO(0));
+        pos = pos && (Dt > 0.0);  // all pivots positive (false on NaN); exact index found in a cold path
       }
     }
-    return;
   }
 
-  // ---------------------------------------------------------------- consumers: one series each
-  const long long b = b0 + tid;
-  const bool valid = b < B;
-  const int lane_leader = (tid & 31) == 0;
-  const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
-  const int TmD = T - D;
+  // ---- cold path (failing series only): 1-based row of the first pivot
+  // D_t <= 0 / non-finite in the chunk starting at t0, by replaying the chunk
+  // from the checkpoint the up sweep stored for it, with exactly the state
+  // restore of the down sweep and the same ldl_step (bitwise-identical).
+  static __device__ __noinline__ int first_bad_row(const Params& p, int c, long long b, const unsigned char* stg,
+                                                   int lane, int t0, int T, double lam_s) {
+    constexpr int NF = Ck<D>::NF;
+    const long long B = p.B;
+    const double* ck = p.ck_f + (long long)c * NF * B + b;
+    const IO* lam_plane = reinterpret_cast<const IO*>(p.lam_plane);
+    FState<D> st;
+    state_init<D>(st);
+    int f = 0;
+    for (int i = 0; i < D; ++i) st.dl[i] = ck[(long long)(f++) * B];
+    for (int m = 0; m < D - 1; ++m)
+      for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = ck[(long long)(f++) * B];
+    for (int i = 0; i < D; ++i) st.v[i] = ck[(long long)(f++) * B];
+    for (int i = 0; i < D; ++i) {
+      const int tj = t0 - 1 - i;
+      const bool in = tj >= 0 && tj < T - D;
+      const double l = !in ? 0.0 : PD ? to_f64<IO>(lam_plane[(long long)tj * B + b]) : lam_s;
+      st.lm[i] = l;
+      st.id[i] = (tj < 0) ? 1.0 : rcp64(l + st.dl[i]);
+    }
+    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;
+    for (int k = 0; k < K && t0 + k < T; ++k) {
+      const int t = t0 + k;
+      const IO wio = t_w[k * 32];
+      const double w = to_f64<IO>(wio);
+      const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : (t < T - D ? lam_s : 0.0);
+      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+      double A[D], Dt, idt, vt;
+      ldl_step<D>(st, w, lt, bb, A, Dt, idt, vt);
+      if (!(Dt > 0.0)) return t + 1;
+    }
+    return 0;
+  }
+
+  // ---- down sweep over one chunk: recompute the factor from the restored state,
+  // then back-substitute rows t0+K-1..t0 and emit outputs.
+  // Outputs of row t0+k go to the warp's staging tiles so0/so1 (row k, this
+  // lane's column); the caller writes them out with TMA stores, which clip
+  // rows past T (z, grad_y) or T-d (D z, grad_lambda) and columns past B.
+  template <bool RAGGED>
+  static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
+                                                    double& lam_acc, const unsigned char* stg, int lane, int t0,
+                                                    int T, double lam_s, IO* so0, IO* so1) {
+    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
+    const IO* t_dz = reinterpret_cast<const IO*>(stg + L::OFF_DZ) + lane;
+    const int TmD = T - D;
+    double q[K];
+    double Ak[K][D];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int t = t0 + k;
+      const IO wio = t_w[k * 32];
+      const double w = to_f64<IO>(wio);
+      double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
+      if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
+      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+      double Dt, idt, vt;
+      ldl_step<D>(st, w, lt, bb, Ak[k], Dt, idt, vt);
+      q[k] = vt * idt;
+      if (RAGGED && t >= T) {  // rows past the end: z = 0 exactly (q = 0, A = 0, zero window)
+        q[k] = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) Ak[k][j] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int k = K - 1; k >= 0; --k) {
+      const int t = t0 + k;
+      double z = q[k];
+#pragma unroll
+      for (int j = 1; j <= D; ++j) {
+        const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
+        z = fma(-Mj(D, j), zw[j - 1], z);
+        z = fma(-a, zw[j - 1], z);
+      }
+      // (D z)_t = sum_j c_j z[t+j]  (rows t <= T-d-1)
+      double dz = Cj(D, 0) * z;
+#pragma unroll
+      for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[j - 1], dz);
+#pragma unroll
+      for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
+      zw[0] = z;
+      if (!BWD) {
+        so0[k * 32] = from_f64<IO>(z);
+        so1[k * 32] = from_f64<IO>(dz);
+      } else {
+        const double w = to_f64<IO>(t_w[k * 32]);
+        so0[k * 32] = from_f64<IO>(w * z);
+        const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
+        if (PD) so1[k * 32] = from_f64<IO>(g);
+        else if (!RAGGED || t < TmD) lam_acc += g;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) cA[i][j] = Ak[i][j];
+  }
+};
+
+// ------------------------------------------------------------------ the kernel
+// One launch = one full forward (BWD=false) or backward (BWD=true).  Each
+// warp owns 32 consecutive series and its own TMA ring: up sweep over C
+// chunks, then down sweep over C chunks in reverse.
+template <int D, typename IO, bool PD, bool BWD>
+__global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid_constant__ Params p) {
+  using L = Layout<D, IO, PD, BWD>;
+  using S = Sweep<D, IO, PD, BWD>;
+  constexpr int K = L::K, ST = L::ST, WARPS = L::WARPS;
   constexpr int NF = Ck<D>::NF, NFAC = Ck<D>::NFAC;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[WARPS][ST];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = p.T, C = p.C;
+  const long long B = p.B;
+  const long long bw = ((long long)blockIdx.x * WARPS + warp) * 32;  // this warp's first series
+  if (bw >= B) return;  // whole warp past the end (no CTA-wide barrier follows)
+  const long long b = bw + lane;
+  const bool valid = b < B;
+  unsigned char* ring = smem + warp * L::WARP_SMEM;
+  IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);
+  IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
+  uint64_t* bars = full_bar[warp];
+  const int ntiles = 2 * C;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < ST && i < ntiles; ++i)
+      issue_tile<D, IO, PD, BWD>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw);
+  }
+  __syncwarp();
+
+  const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
+  const int cr = (T - D) / K;  // first chunk that reaches row T-D (ragged handling from there on)
 
   FState<D> st;
   state_init<D>(st);
   int nobs = 0, bad = 0;
-  int it = 0;  // tile sequence index (ring position)
+  int it = 0;
 
   // ================================================================ up sweep
   for (int c = 0; c < C; ++c, ++it) {
     const int s = it % ST;
-    mbar_wait(&full_bar[s], (uint32_t)((it / ST) & 1));
-    const unsigned char* stg = smem + s * L::STAGE;
-    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + tid;
-    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + tid;
-    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + tid;
+    mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
+    const unsigned char* stg = ring + s * L::STAGE;
     const int t0 = c * K;
-    // checkpoint: state entering row t0
-    if (valid) {
+    if (valid) {  // checkpoint: state entering row t0
       if (!BWD) {
         double* ck = p.ck_f + (long long)c * NF * B + b;
         int f = 0;
@@ -315,25 +481,21 @@ __global__ void __maxnreg__((Tile<IO, D>::MAXREG)) whit_kernel(const __grid_cons
         for (int i = 0; i < D; ++i) ck[(long long)i * B] = st.v[i];
       }
     }
-    const int n = min(K, T - t0);
-#pragma unroll 4
-    for (int k = 0; k < n; ++k) {
-      const int t = t0 + k;
-      const double rhs = to_f64<IO>(t_rhs[k * NT]);
-      const double w = to_f64<IO>(t_w[k * NT]);
-      const double lt = PD ? to_f64<IO>(t_lam[k * NT]) : (t < TmD ? lam_s : 0.0);
-      const double bb = BWD ? rhs : (w != 0.0 ? w * rhs : 0.0);
-      double A[D], Dt, idt, vt;
-      ldl_step<D>(st, w, lt, bb, A, Dt, idt, vt);
-      if (!BWD) {
-        nobs += (w > 0.0);
-        if (bad == 0 && !(Dt > 0.0)) bad = t + 1;  // also catches NaN
-      }
-    }
+    bool pos = true;
+    if (c < cr) S::template up_chunk<false>(st, stg, lane, t0, T, lam_s, nobs, pos);
+    else S::template up_chunk<true>(st, stg, lane, t0, T, lam_s, nobs, pos);
+    if (!BWD && !pos && bad == 0 && valid) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s);
     __syncwarp();
-    if (lane_leader) mbar_arrive(&empty_bar[s]);
+    if (lane == 0 && it + ST < ntiles) {
+      fence_proxy_async_smem();
+      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw);
+    }
   }
 
+  // Status (LAPACK xPBTRF style): fewer than d observed days -> T-d+1 (exactly
+  // singular for lambda > 0); else first non-positive pivot row.  A failed
+  // series is poisoned with NaN in the restored rhs state, so every output
+  // derived from it (z, D z, w*u, -(D u)(D z)) is NaN without per-store checks.
   bool failed;
   if (!BWD) {
     const int info = (nobs < D) ? (T - D + 1) : bad;
@@ -342,7 +504,7 @@ __global__ void __maxnreg__((Tile<IO, D>::MAXREG)) whit_kernel(const __grid_cons
   } else {
     failed = valid ? (p.info[b] != 0) : true;
   }
-  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  const double poison = failed ? qnan() : 0.0;
 
   // ================================================================ down sweep
   double cA[D][D];  // A[t0+K+i][j+1] of the chunk processed before (later in time)
@@ -355,37 +517,29 @@ __global__ void __maxnreg__((Tile<IO, D>::MAXREG)) whit_kernel(const __grid_cons
   }
   double lam_acc = 0.0;  // scalar-lambda gradient accumulator
 
-  // checkpoint prefetch registers
+  // checkpoint prefetch registers (next chunk to process)
   double pdl[D], pap[NFAC - D > 0 ? NFAC - D : 1], pv[D];
-  auto load_ck = [&](int c) {
-    if (!valid) return;
-    const double* ckf = p.ck_f + (long long)c * NF * B + b;
-#pragma unroll
-    for (int i = 0; i < D; ++i) pdl[i] = ckf[(long long)i * B];
-#pragma unroll
-    for (int f = 0; f < NFAC - D; ++f) pap[f] = ckf[(long long)(D + f) * B];
-    if (!BWD) {
-#pragma unroll
-      for (int i = 0; i < D; ++i) pv[i] = ckf[(long long)(NFAC + i) * B];
-    } else {
-      const double* ckb = p.ck_b + (long long)c * D * B + b;
-#pragma unroll
-      for (int i = 0; i < D; ++i) pv[i] = ckb[(long long)i * B];
-    }
-  };
-  load_ck(C - 1);
-
-  IO* out0 = reinterpret_cast<IO*>(p.out0);
-  IO* out1 = reinterpret_cast<IO*>(p.out1);
+#define WHIT_LOAD_CK(cc)                                                                          \
+  do {                                                                                            \
+    if (valid) {                                                                                  \
+      const double* ckf = p.ck_f + (long long)(cc) * NF * B + b;                                  \
+      _Pragma("unroll") for (int i = 0; i < D; ++i) pdl[i] = ckf[(long long)i * B];               \
+      _Pragma("unroll") for (int f = 0; f < NFAC - D; ++f) pap[f] = ckf[(long long)(D + f) * B];  \
+      if (!BWD) {                                                                                 \
+        _Pragma("unroll") for (int i = 0; i < D; ++i) pv[i] = ckf[(long long)(NFAC + i) * B];     \
+      } else {                                                                                    \
+        const double* ckb = p.ck_b + (long long)(cc) * D * B + b;                                 \
+        _Pragma("unroll") for (int i = 0; i < D; ++i) pv[i] = ckb[(long long)i * B];              \
+      }                                                                                           \
+    }                                                                                             \
+  } while (0)
+  WHIT_LOAD_CK(C - 1);
 
   for (int c = C - 1; c >= 0; --c, ++it) {
     const int s = it % ST;
-    mbar_wait(&full_bar[s], (uint32_t)((it / ST) & 1));
-    const unsigned char* stg = smem + s * L::STAGE;
-    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + tid;
-    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + tid;
-    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + tid;  // row k <-> t0 - D + k
-    const IO* t_dz = reinterpret_cast<const IO*>(stg + L::OFF_DZ) + tid;
+    mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
+    const unsigned char* stg = ring + s * L::STAGE;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
     const int t0 = c * K;
 
     // restore the state entering row t0 from the checkpoint
@@ -399,80 +553,36 @@ __global__ void __maxnreg__((Tile<IO, D>::MAXREG)) whit_kernel(const __grid_cons
       for (int i = 0; i < D; ++i) {
         const int tj = t0 - 1 - i;
         st.dl[i] = pdl[i];
-        st.v[i] = pv[i];
-        const double l = PD ? to_f64<IO>(t_lam[(D - 1 - i) * NT]) : ((tj >= 0 && tj < TmD) ? lam_s : 0.0);
+        st.v[i] = pv[i] + poison;
+        const double l = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : ((tj >= 0 && tj < T - D) ? lam_s : 0.0);
         st.lm[i] = l;
         st.id[i] = (tj < 0) ? 1.0 : rcp64(l + pdl[i]);
       }
     }
-    if (c > 0) load_ck(c - 1);
+    if (c > 0) WHIT_LOAD_CK(c - 1);
 
-    // recompute the chunk's factor into registers
-    double q[K];
-    double Ak[K][D];
-    const bool ragged = (t0 + K > T);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int t = t0 + k;
-      if (ragged && t >= T) {
-        q[k] = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) Ak[k][j] = 0.0;
-        continue;
-      }
-      const double rhs = to_f64<IO>(t_rhs[k * NT]);
-      const double w = to_f64<IO>(t_w[k * NT]);
-      const double lt = PD ? to_f64<IO>(t_lam[(k + D) * NT]) : (t < TmD ? lam_s : 0.0);
-      const double bb = BWD ? rhs : (w != 0.0 ? w * rhs : 0.0);
-      double Dt, idt, vt;
-      ldl_step<D>(st, w, lt, bb, Ak[k], Dt, idt, vt);
-      q[k] = vt * idt;
-    }
-
-    // back substitution over the chunk, descending
-#pragma unroll
-    for (int k = K - 1; k >= 0; --k) {
-      const int t = t0 + k;
-      if (ragged && t >= T) continue;
-      double z = q[k];
-#pragma unroll
-      for (int j = 1; j <= D; ++j) {
-        const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
-        z = fma(-Mj(D, j), zw[j - 1], z);
-        z = fma(-a, zw[j - 1], z);
-      }
-      // (D z)_t = sum_j c_j z[t+j]  (rows t <= T-d-1)
-      double dz = Cj(D, 0) * z;
-#pragma unroll
-      for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[j - 1], dz);
-#pragma unroll
-      for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
-      zw[0] = z;
-      if (valid) {
-        const long long idx = (long long)t * B + b;
-        if (!BWD) {
-          out0[idx] = from_f64<IO>(failed ? qnan : z);
-          if (t < TmD) out1[idx] = from_f64<IO>(failed ? qnan : dz);
-        } else {
-          const double w = to_f64<IO>(t_w[k * NT]);
-          out0[idx] = from_f64<IO>(failed ? qnan : w * z);
-          if (t < TmD) {
-            const double g = -dz * to_f64<IO>(t_dz[k * NT]);
-            if (PD) out1[idx] = from_f64<IO>(failed ? qnan : g);
-            else lam_acc += g;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) cA[i][j] = Ak[i][j];
-
+    // the staging tiles must have been read by the previous chunk's TMA stores
+    if (lane == 0) bulk_wait_read0();
     __syncwarp();
-    if (lane_leader) mbar_arrive(&empty_bar[s]);
+    if (c < cr)
+      S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane);
+    else
+      S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane);
+    fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(&p.tm_out0, so0, (int)bw, t0);
+      if (!BWD || PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
+      bulk_commit();
+    }
+    if (lane == 0 && it + ST < ntiles) {
+      fence_proxy_async_smem();
+      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw);
+    }
   }
-  if (BWD && !PD && valid) out1[b] = from_f64<IO>(failed ? qnan : lam_acc);
+#undef WHIT_LOAD_CK
+  if (lane == 0) bulk_wait0();  // stores complete before the CTA exits (smem stays valid)
+  if (BWD && !PD && valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc);
 }
 
 // Count of failed series (info != 0) for whit_failures.

@@ -11,11 +11,14 @@ import numpy as np
 
 
 def rel_series(a, ref, denom=None):
+    """Per-series max-abs error over the last axis / denom (default max|ref| of the series).
+    A 1-D input is ONE series; a 0-d input is a scalar per series."""
     a = np.asarray(a, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
+    if a.ndim == 0:
+        a, ref = a[None], ref[None]
     if a.ndim == 1:
-        a, ref = a[:, None], ref[:, None]
-        denom = None if denom is None else np.asarray(denom)
+        a, ref = a[None, :], ref[None, :]
     err = np.max(np.abs(a - ref), axis=-1)
     den = np.max(np.abs(ref), axis=-1) if denom is None else np.asarray(denom, dtype=np.float64)
     den = np.where(den > 0, den, 1.0)
