@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark of the Whittaker hot path (BASELINE.json metric) on 1..N B200s.
+
+A step = one forward (whit_forward) + one backward (whit_backward) over the
+whole per-GPU batch of the 'hetero' workload (BASELINE.json configs[2]:
+262,144 series x T = 3,288 daily steps, d = 2, per-date lambda, fp32 I/O,
+fp64 arithmetic).  Multi-GPU: one process per GPU (torchrun), each rank
+solves its own shard of independent series (weak scaling, no data-path
+collective; torch.distributed/NCCL only for the barrier and the max-over-
+ranks timing).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle
+(oracle/, test infrastructure) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "series fwd+bwd solves/s (T=3288, d=2, per-date λ) and % of HBM peak, 1/2/4/8 GPU"
+UNIT = "series/s"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="libwhit", choices=["libwhit", "reference"])
+    ap.add_argument("--config", default="hetero", choices=["hetero", "homo", "toy"])
+    ap.add_argument("--io", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="series in the CPU-oracle sample (0 = auto)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = float(json.load(open(p))["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs, copy r+w)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int, period_ms: int = 50):
+        self.dev = device_index
+        self.period = period_ms
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.dev), f"-lms={self.period}"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=1)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(B: int, T: int, d: int, esz: int, per_date: bool, K: int = 16):
+    """Bytes each launch must move in the R-mode design: inputs read in the
+    up sweep and re-read in the down sweep, outputs written once, fp64 checkpoints."""
+    C = math.ceil(T / K)
+    nfac, nrhs = d + d * (d - 1) // 2, d
+    lam_rows = (T - d) if per_date else 0
+    fwd = (2 * (2 * T + lam_rows) * esz            # y, w (+ lambda) read twice
+           + (T + (T - d)) * esz                    # z, D z written
+           + 2 * C * (nfac + nrhs) * 8              # checkpoints written + read
+           + (0 if per_date else esz)) * B          # scalar lambda
+    bwd = (2 * (2 * T + lam_rows) * esz            # g, w (+ lambda) read twice
+           + (T - d) * esz                          # D z read
+           + T * esz + (lam_rows * esz if per_date else esz)  # grad_y, grad_lambda written
+           + C * nrhs * 8 * 2                       # rhs checkpoints written + read
+           + C * nfac * 8                           # factor checkpoints read
+           + (0 if per_date else esz) + 4) * B      # scalar lambda, info
+    minimum_fwd = ((2 * T + lam_rows) * esz + (2 * T - d) * esz) * B   # single read + z + D z
+    minimum_bwd = ((2 * T + lam_rows) * esz + (T - d) * esz + (T + lam_rows) * esz) * B
+    return fwd, bwd, minimum_fwd, minimum_bwd
+
+
+def load_profile_traffic():
+    """dram bytes/launch from the committed ncu --set full summary (profiles/), if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+def _oracle_one(args):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    y, w, lam, g, d = args
+    from oracle import whittaker as O1
+    t = time.perf_counter()
+    O1.forward_backward(y, w, lam, d, g)
+    return time.perf_counter() - t
+
+
+def oracle_pool(cores: int):
+    import multiprocessing as mp
+    os.environ.update({"OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"})
+    pool = mp.get_context("spawn").Pool(cores)
+    pool.map(_oracle_warm, range(cores))  # import numpy/scipy/oracle in every worker, untimed
+    return pool
+
+
+def _oracle_warm(_):
+    import oracle  # noqa: F401
+    return 0
+
+
+def oracle_rate(hin: dict, n: int, d: int, pool):
+    """fwd+bwd series/s of the CPU oracle (O1 dense + refinement) over n series on the pool's processes."""
+    items = [(hin["y"][i], hin["w"][i], hin["lam"][i], hin["g"][i], d) for i in range(n)]
+    t0 = time.perf_counter()
+    per = pool.map(_oracle_one, items, chunksize=1)
+    wall = time.perf_counter() - t0
+    return n / wall, wall, sum(per)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def sample_host_inputs(x: dict, n: int):
+    """n series spread over the shard, copied to host (series-major float64)."""
+    import numpy as np
+    import torch
+    B = x["y"].shape[1]
+    idx = torch.linspace(0, B - 1, n).long().to(x["y"].device)
+    out = {}
+    for k in ("y", "w", "lam", "g"):
+        v = x[k]
+        v = v[:, idx] if v.dim() == 2 else v[idx]
+        a = v.double().cpu().numpy()
+        out[k] = np.ascontiguousarray(a.T) if a.ndim == 2 else a
+    return out
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    cores = min(host_cores(), 32)
+    n = args.cpu_sample or cores
+    # the same workload's series (global ids spread over the batch), generated on the host
+    ids = torch.linspace(0, cfg.B - 1, n).long()
+    x = synth.make_inputs(cfg, device="cpu", dtype=torch.float32 if args.io == "f32" else torch.float64,
+                          series_ids=ids)
+    hin = sample_host_inputs(x, n)
+    pool = oracle_pool(cores)
+    for _ in range(args.warmup):
+        oracle_rate(hin, min(n, cores), cfg.d, pool)
+    rates, walls = [], []
+    for _ in range(args.steps):
+        r, wall, _cpu = oracle_rate(hin, n, cfg.d, pool)
+        rates.append(r)
+        walls.append(wall)
+    pool.close()
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": statistics.median(walls) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "B": cfg.B, "T": cfg.T, "d": cfg.d, "lambda": cfg.lam_mode,
+                   "io": args.io, "sample_series_per_step": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"{n} series of the {args.config} workload per step, O1 dense fp64 + 2 long-double "
+                                   f"refinement steps, fwd+bwd, {cores} processes"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- libwhit arm
+def run_libwhit(args):
+    import torch
+    import torch.distributed as dist
+
+    ws_n, rank, local = dist_env()
+    if ws_n != args.gpus:
+        if ws_n == 1 and args.gpus > 1:
+            print(json.dumps({"error": f"--gpus {args.gpus} needs torchrun with {args.gpus} processes"}))
+            return 2
+    if ws_n > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if ws_n > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    import paper_2604_00048_b200 as P
+    import synth
+
+    cfg = synth.CONFIGS[args.config]
+    io = torch.float32 if args.io == "f32" else torch.float64
+    esz = 4 if io == torch.float32 else 8
+    B, T, d = cfg.B, cfg.T, cfg.d
+    per_date = cfg.lam_mode == "per_date"
+    x = synth.make_inputs(cfg, B=B, series_offset=rank * B, device=dev, dtype=io)
+    y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
+    stream = torch.cuda.current_stream(dev)
+    wsp = P.Workspace(d, T, B, io, per_date, device=dev, stream=stream)
+    z = torch.empty_like(y)
+    gy = torch.empty_like(y)
+    gl = torch.empty_like(lam)
+
+    def step():
+        P.whit_forward(y, w, lam, d, T, B, z, wsp)
+        P.whit_backward(g, wsp, z, gy, gl)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    nfail = P.whit_failures(wsp)
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(dev.index if dev.index is not None else 0)
+    if ws_n > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk.start()
+    time.sleep(0.15)  # let the sampler attach before the timed region
+    t_start.record(stream)
+    for i in range(K):
+        ev[i][0].record(stream)
+        P.whit_forward(y, w, lam, d, T, B, z, wsp)
+        ev[i][1].record(stream)
+        P.whit_backward(g, wsp, z, gy, gl)
+        ev[i][2].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if ws_n > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ms_step = total_ms / K
+    if ws_n > 1:
+        tt = torch.tensor([ms_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+    value = ws_n * B / (ms_step / 1e3)
+
+    # roofline of the dominant kernel
+    fb, bb, mf, mb = algorithmic_bytes(B, T, d, esz, per_date)
+    f_avg, b_avg = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
+    dom = "whit_backward" if b_avg >= f_avg else "whit_forward"
+    dom_ms, dom_bytes, dom_min = (b_avg, bb, mb) if dom == "whit_backward" else (f_avg, fb, mf)
+    peak, peak_src = measured_peak_gbs()
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    prof = load_profile_traffic() or {}
+    traffic = prof.get(dom, {}).get("dram_bytes_per_launch") if isinstance(prof.get(dom), dict) else None
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": dom, "kernel_ms": round(dom_ms, 4), "algorithmic_bytes": dom_bytes,
+            "minimum_bytes": dom_min, "peak_source": peak_src,
+            "traffic_source": prof.get("source") if traffic is not None else None,
+            "fwd_ms": round(f_avg, 4), "bwd_ms": round(b_avg, 4),
+            "step_GBps_algorithmic": round((fb + bb) / (ms_step / 1e3) / 1e9, 1),
+            "step_frac_of_min_bytes": round((mf + mb) / (ms_step / 1e3) / 1e9 / peak, 4)}
+
+    # end to end through the public API with host buffers (rank-local)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(P, wsp, x, z, gy, gl, d, T, B, io, stream, dev, args.e2e_steps, ws_n)
+
+    # CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws_n == 1 and not args.no_cpu_baseline:
+        cores = min(host_cores(), 32)
+        n = args.cpu_sample or 2 * cores
+        hin = sample_host_inputs(x, n)
+        pool = oracle_pool(cores)
+        rate, wall, cpu_s = oracle_rate(hin, n, d, pool)
+        pool.close()
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{n} series of this workload (spread over the batch), O1 dense fp64 + long-double "
+                         f"refinement, fwd+bwd, {cores} processes, {wall:.1f} s wall / {cpu_s:.1f} s CPU"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws_n, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "B_per_gpu": B, "T": T, "d": d, "lambda": cfg.lam_mode,
+                       "io": args.io, "global_batch": ws_n * B, "parallelism": f"dp{ws_n}",
+                       "l2": "inputs larger than L2 (each [T][B] plane %.2f GB vs 126 MB L2)" % (T * B * esz / 1e9),
+                       "mask": "Sentinel-2 revisit + seasonal clouds, 90-day trailing gap",
+                       "failed_series": nfail},
+            "roofline": roof, "gpu_launches": 2 * K, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws_n > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(P, wsp, x, z, gy, gl, d, T, B, io, stream, dev, steps, ws_n):
+    """Same metric through the public API with pinned HOST buffers: each step copies y, w,
+    lambda, g host->device, runs whit_forward + whit_backward, and copies z, grad_y,
+    grad_lambda device->host."""
+    import torch
+    hy = torch.empty(x["y"].shape, dtype=io, pin_memory=True)
+    hw = torch.empty(x["w"].shape, dtype=io, pin_memory=True)
+    hl = torch.empty(x["lam"].shape, dtype=io, pin_memory=True)
+    hg = torch.empty(x["g"].shape, dtype=io, pin_memory=True)
+    for h, k in ((hy, "y"), (hw, "w"), (hl, "lam"), (hg, "g")):
+        h.copy_(x[k])
+    oz = torch.empty(z.shape, dtype=io, pin_memory=True)
+    oy = torch.empty(gy.shape, dtype=io, pin_memory=True)
+    ol = torch.empty(gl.shape, dtype=io, pin_memory=True)
+    dy, dw, dl, dg = (torch.empty_like(x[k]) for k in ("y", "w", "lam", "g"))
+    h2d = sum(t.numel() * t.element_size() for t in (hy, hw, hl, hg))
+    d2h = sum(t.numel() * t.element_size() for t in (oz, oy, ol))
+
+    def step():
+        dy.copy_(hy, non_blocking=True)
+        dw.copy_(hw, non_blocking=True)
+        dl.copy_(hl, non_blocking=True)
+        dg.copy_(hg, non_blocking=True)
+        P.whit_forward(dy, dw, dl, d, T, B, z, wsp)
+        P.whit_backward(dg, wsp, z, gy, gl)
+        oz.copy_(z, non_blocking=True)
+        oy.copy_(gy, non_blocking=True)
+        ol.copy_(gl, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    if ws_n > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"value": ws_n * B / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": ms, "steps": steps}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_libwhit(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -113,8 +113,9 @@ def make_inputs(cfg: Config | str, *, B: int | None = None, T: int | None = None
                 d: int | None = None, seed: int | None = None, series_offset: int = 0,
                 device="cpu", dtype=torch.float32, with_g: bool = True,
                 lam_mode: str | None = None, mask: str | None = None,
-                lam_max: float = 1e5, row_chunk_elems: int = 1 << 24) -> dict:
-    """Draw one shard ``[series_offset, series_offset + B)`` of a config.
+                lam_max: float = 1e5, row_chunk_elems: int = 1 << 24, series_ids=None) -> dict:
+    """Draw one shard ``[series_offset, series_offset + B)`` of a config (or the
+    explicit global ``series_ids``, e.g. a sample spread over the batch).
 
     Returns ``{"y": (T,B), "w": (T,B), "lam": (T-d,B) or (B,), "g": (T,B)}`` on
     ``device`` in ``dtype`` (float32 or float64), plus the config echo.
@@ -128,7 +129,11 @@ def make_inputs(cfg: Config | str, *, B: int | None = None, T: int | None = None
     mask = cfg.mask if mask is None else mask
     seed = BASE_SEED + cfg.seed_offset if seed is None else seed
     dev = torch.device(device)
-    ser = torch.arange(series_offset, series_offset + B, dtype=torch.int64, device=dev)
+    if series_ids is not None:
+        ser = torch.as_tensor(series_ids, dtype=torch.int64, device=dev)
+        B = int(ser.numel())
+    else:
+        ser = torch.arange(series_offset, series_offset + B, dtype=torch.int64, device=dev)
     S = _Stream(seed, ser)
 
     # per-series parameters
