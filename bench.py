@@ -55,6 +55,22 @@ def dist_env():
     return ws, rank, local
 
 
+def shard(rank: int, world: int, B_per_rank: int):
+    """Weak scaling: rank r owns the global series [r*B, (r+1)*B) (contiguous, disjoint)."""
+    return rank * B_per_rank, B_per_rank
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """Max of a per-rank scalar over the default process group (identity without one)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measured_peak_gbs():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -270,7 +286,8 @@ def run_libwhit(args):
     esz = 4 if io == torch.float32 else 8
     B, T, d = cfg.B, cfg.T, cfg.d
     per_date = cfg.lam_mode == "per_date"
-    x = synth.make_inputs(cfg, B=B, series_offset=rank * B, device=dev, dtype=io)
+    off, B = shard(rank, ws_n, B)
+    x = synth.make_inputs(cfg, B=B, series_offset=off, device=dev, dtype=io)
     y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
     stream = torch.cuda.current_stream(dev)
     wsp = P.Workspace(d, T, B, io, per_date, device=dev, stream=stream)
@@ -311,11 +328,7 @@ def run_libwhit(args):
     total_ms = t_start.elapsed_time(t_end)
     fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
     bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    ms_step = total_ms / K
-    if ws_n > 1:
-        tt = torch.tensor([ms_step], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_step = float(tt.item())
+    ms_step = max_over_ranks(total_ms / K, dev)
     value = ws_n * B / (ms_step / 1e3)
 
     # roofline of the dominant kernel
@@ -409,12 +422,7 @@ def run_e2e(P, wsp, x, z, gy, gl, d, T, B, io, stream, dev, steps, ws_n):
         step()
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / steps
-    if ws_n > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / steps, dev)
     return {"value": ws_n * B / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": ms, "steps": steps}
 

@@ -1,0 +1,61 @@
+"""Multi-process (world size 2, gloo, CPU) coverage of the bench's multi-GPU host logic:
+weak-scaling shards, max-over-ranks timing, and rank-independence of each series' inputs
+(inputs keyed on the global series id, so per-series results cannot depend on N)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    import synth
+    off, B = bench.shard(rank, world, 64)
+    # max over ranks of a per-rank "step time"
+    mx = bench.max_over_ranks(1.5 + rank)
+    # this rank's shard of the hetero workload (short T to keep it quick)
+    x = synth.make_inputs("hetero", B=B, T=80, series_offset=off)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (off, B, {k: x[k].clone() for k in ("y", "w", "lam", "g")}))
+    if rank == 0:
+        q.put((mx, gathered))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_world2_shards_timing_and_rank_independent_inputs():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    mx, gathered = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert mx == 2.5
+    (o0, b0, x0), (o1, b1, x1) = gathered
+    assert (o0, b0, o1, b1) == (0, 64, 64, 64)  # contiguous, disjoint, covering [0, 128)
+    import synth
+    full = synth.make_inputs("hetero", B=128, T=80)
+    for k in ("y", "w", "lam", "g"):
+        assert torch.equal(torch.cat([x0[k], x1[k]], dim=-1), full[k]), k
+
+
+def test_max_over_ranks_without_group_is_identity():
+    import bench
+    assert bench.max_over_ranks(3.25) == 3.25
