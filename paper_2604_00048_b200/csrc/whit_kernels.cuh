@@ -115,17 +115,23 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// fp64 reciprocal: MUFU.RCP64H seed + 2 Newton steps (error ~1 ulp).  Used
-// identically by every sweep so recomputed factors are bitwise identical.
+// fp64 reciprocal: MUFU.RCP64H seed (~2^-22) + NEWTON Newton steps.  Two steps
+// give ~1 ulp (fp64 I/O: the 1e-10 target); one step gives ~2^-44 relative,
+// ~1e4x below what the fp32-I/O tolerances can see, and shortens the
+// per-row dependency chain by two DFMAs.  Every sweep uses the identical
+// sequence, so recomputed factors are bitwise identical.
+template <int NEWTON>
 __device__ __forceinline__ double rcp64(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
+#pragma unroll
+  for (int i = 0; i < NEWTON; ++i) {
+    const double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+  }
   return r;
 }
+template <typename IO> struct Newton { static constexpr int N = sizeof(IO) == 4 ? 1 : 2; };
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000LL); }
 
@@ -172,7 +178,11 @@ template <int D> __device__ __forceinline__ void state_init(FState<D>& s) {
 // Outputs A[0..D-1] (= A_{t,1..D}), D_t, 1/D_t, v_t; advances the state.
 // Terms with E_D = 0 are dropped at compile time (an fma with a zero operand
 // is not foldable under IEEE rules, so it must not be written).
-template <int D>
+//
+// Accumulation order is chosen for latency: terms are added from j = D down to
+// j = 1 so that A_1 (the last-computed, on the loop-carried chain
+// Delta_{t-1} -> 1/D_{t-1} -> A_{t,1} -> Delta_t) enters last.
+template <int D, int NEWTON>
 __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, double b, double (&A)[D],
                                          double& Dt, double& idt, double& vt) {
   double E[D + 1];
@@ -194,17 +204,17 @@ __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, d
   }
   double dl = w;
 #pragma unroll
-  for (int j = 1; j < D; ++j) dl = fma(-Mj(D, j), E[j], dl);
+  for (int j = D - 1; j >= 1; --j) dl = fma(-Mj(D, j), E[j], dl);
 #pragma unroll
-  for (int j = 1; j <= D; ++j) {
+  for (int j = D; j >= 1; --j) {
     const double inner = (j < D) ? fma(Mj(D, j), s.lm[j - 1], E[j]) : Mj(D, j) * s.lm[j - 1];
     dl = fma(-A[j - 1], inner, dl);
   }
   Dt = lam_t + dl;
-  idt = rcp64(Dt);
+  idt = rcp64<NEWTON>(Dt);
   double v = b;
 #pragma unroll
-  for (int j = 1; j <= D; ++j) {
+  for (int j = D; j >= 1; --j) {
     v = fma(-Mj(D, j), s.v[j - 1], v);
     v = fma(-A[j - 1], s.v[j - 1], v);
   }
@@ -231,14 +241,14 @@ template <int D> struct Ck {
 // One warp = 32 series = one TMA pipeline.  K time steps per chunk/tile, ST
 // ring stages per warp, WARPS warps per CTA.  K = 16 for d <= 2; d = 3 keeps
 // 4 fp64 values per chunk row in registers, so its chunk is 8 steps.
-// Registers are allocated per pair of warps, so CTAs are 4 warps; the forward
-// runs 3 CTAs (12 warps, <= 168 regs) per SM, the backward (one more staged
-// input plane) 2 CTAs (8 warps, <= 255 regs) so its rings fit in 227 KB.
+// Registers are allocated per pair of warps.  Forward: 4-warp CTAs, 3 per SM
+// (12 warps, <= 168 regs, 16.8 KB smem per warp).  Backward (one more staged
+// input plane, 21 KB per warp): 2-warp CTAs, 5 per SM (10 warps, <= 200 regs).
 template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int K = D <= 2 ? 16 : 8;
   static constexpr int ST = 2;
-  static constexpr int WARPS = 4;
-  static constexpr int MAXREG = (BWD || sizeof(IO) == 8) ? 255 : 168;
+  static constexpr int WARPS = BWD ? 2 : 4;
+  static constexpr int MAXREG = BWD ? 200 : 168;
 };
 
 template <int D, typename IO, bool PD, bool BWD> struct Layout {
@@ -298,7 +308,7 @@ struct Sweep {
       if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double A[D], Dt, idt, vt;
-      ldl_step<D>(st, w, lt, bb, A, Dt, idt, vt);
+      ldl_step<D, Newton<IO>::N>(st, w, lt, bb, A, Dt, idt, vt);
       if (!BWD) {
         nobs += (wio > IO(0));
         pos = pos && (Dt > 0.0);  // all pivots positive (false on NaN); exact index found in a cold path
@@ -328,7 +338,7 @@ struct Sweep {
       const bool in = tj >= 0 && tj < T - D;
       const double l = !in ? 0.0 : PD ? to_f64<IO>(lam_plane[(long long)tj * B + b]) : lam_s;
       st.lm[i] = l;
-      st.id[i] = (tj < 0) ? 1.0 : rcp64(l + st.dl[i]);
+      st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO>::N>(l + st.dl[i]);
     }
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
@@ -340,7 +350,7 @@ struct Sweep {
       const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : (t < T - D ? lam_s : 0.0);
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double A[D], Dt, idt, vt;
-      ldl_step<D>(st, w, lt, bb, A, Dt, idt, vt);
+      ldl_step<D, Newton<IO>::N>(st, w, lt, bb, A, Dt, idt, vt);
       if (!(Dt > 0.0)) return t + 1;
     }
     return 0;
@@ -371,7 +381,7 @@ struct Sweep {
       if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double Dt, idt, vt;
-      ldl_step<D>(st, w, lt, bb, Ak[k], Dt, idt, vt);
+      ldl_step<D, Newton<IO>::N>(st, w, lt, bb, Ak[k], Dt, idt, vt);
       q[k] = vt * idt;
       if (RAGGED && t >= T) {  // rows past the end: z = 0 exactly (q = 0, A = 0, zero window)
         q[k] = 0.0;
@@ -384,7 +394,7 @@ struct Sweep {
       const int t = t0 + k;
       double z = q[k];
 #pragma unroll
-      for (int j = 1; j <= D; ++j) {
+      for (int j = D; j >= 1; --j) {  // z[t+1] (just computed) enters last
         const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
         z = fma(-Mj(D, j), zw[j - 1], z);
         z = fma(-a, zw[j - 1], z);
@@ -400,11 +410,17 @@ struct Sweep {
         so0[k * 32] = from_f64<IO>(z);
         so1[k * 32] = from_f64<IO>(dz);
       } else {
-        const double w = to_f64<IO>(t_w[k * 32]);
-        so0[k * 32] = from_f64<IO>(w * z);
-        const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
-        if (PD) so1[k * 32] = from_f64<IO>(g);
-        else if (!RAGGED || t < TmD) lam_acc += g;
+        if (sizeof(IO) == 4 && PD) {
+          // fp32 I/O: w*u and -(Du)(Dz) formed from u, Du rounded once to fp32 (<= 1.5 ulp fp32)
+          so0[k * 32] = t_w[k * 32] * from_f64<IO>(z);
+          so1[k * 32] = -(from_f64<IO>(dz) * t_dz[k * 32]);  // D z tile is 0 past row T-d-1
+        } else {
+          const double w = to_f64<IO>(t_w[k * 32]);
+          so0[k * 32] = from_f64<IO>(w * z);
+          const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
+          if (PD) so1[k * 32] = from_f64<IO>(g);
+          else if (!RAGGED || t < TmD) lam_acc += g;
+        }
       }
     }
 #pragma unroll
@@ -556,7 +572,7 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
         st.v[i] = pv[i] + poison;
         const double l = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : ((tj >= 0 && tj < T - D) ? lam_s : 0.0);
         st.lm[i] = l;
-        st.id[i] = (tj < 0) ? 1.0 : rcp64(l + pdl[i]);
+        st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO>::N>(l + pdl[i]);
       }
     }
     if (c > 0) WHIT_LOAD_CK(c - 1);

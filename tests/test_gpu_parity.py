@@ -29,6 +29,10 @@ def oracle_O2(h, d):
     if "g" in h:
         yb, lb = O2.backward_banded(h["g"], h["w"], lam, d, z)
         out.update(ybar=yb, lambar=lb)
+        if np.asarray(lam).ndim == 1:  # scalar lambda: also the summands -(Du)_r (Dz)_r of lambar
+            T = h["y"].shape[1]
+            _, terms = O2.backward_banded(h["g"], h["w"], np.repeat(np.asarray(lam)[:, None], T - d, 1), d, z)
+            out["lambar_abs_terms"] = np.sum(np.abs(terms.astype(np.float64)), axis=1)
     return out
 
 
@@ -42,9 +46,12 @@ def check(res, ref, h, d, dtype, backward=True, idx=None, label=""):
     if backward:
         ey = rel_series(res["ybar"][sl], ref["ybar"])
         rl, fl = np.asarray(res["lambar"][sl]), np.asarray(ref["lambar"])
-        if rl.ndim == 1:  # scalar lambda: one gradient per series, relative error each
-            rl, fl = rl[:, None], fl[:, None]
-        el = rel_series(rl, fl)
+        if rl.ndim == 1:  # scalar lambda: one gradient per series, a sum over r (R-9: relative to
+            # sum_r |-(Du)_r (Dz)_r| when the summands are known, i.e. the condition of the sum)
+            den = ref.get("lambar_abs_terms")
+            el = rel_series(rl[:, None], fl[:, None], den)
+        else:
+            el = rel_series(rl, fl)
         assert ey.max() <= tg, f"{label} ybar err {ey.max():.3e}"
         assert el.max() <= tg, f"{label} lambar err {el.max():.3e}"
     return ez.max()
