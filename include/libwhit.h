@@ -159,6 +159,39 @@ whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info);
  * consume it on the device without a synchronisation. */
 const int32_t* whit_info_device(const whit_ws* ws);
 
+/* ---------------------------------------------------------------------------
+ * Streaming executor for data in HOST memory.
+ *
+ * Runs the forward (and, if grad_z != NULL, the backward) over B series whose
+ * planes live in HOST memory in the same [T][B] layout, streaming them through
+ * the GPU in series chunks of `chunk` columns on `nbuf` device slots with one
+ * stream each: pitched 2-D host->device copies of the chunk, whit_forward /
+ * whit_backward, pitched 2-D device->host copies of z, grad_y, grad_lambda and
+ * (if info != NULL) the chunk's info.  Slots overlap, so copies in both
+ * directions run concurrently with the kernels.  Same arithmetic and results
+ * as the device entry points (each chunk is an independent batch).
+ *
+ *   y, w, lambda, grad_z   HOST inputs ([T][B], [T][B], [T-d][B] or [B], [T][B])
+ *   z, grad_y, grad_lambda HOST outputs (grad_* ignored when grad_z == NULL)
+ *   info                   optional HOST int32[B] (LAPACK-style status, see above)
+ *   chunk, nbuf            series per chunk (multiple of 4 for F32, 2 for F64),
+ *                          device slots in flight (1..8; 3 recommended)
+ *   dev_buf, dev_bytes     caller-owned device scratch, >= whit_host_ws_bytes(),
+ *                          256-B aligned
+ *   cuda_stream            the call is ordered after prior work on this stream
+ *                          and later work on it waits for completion; the host
+ *                          call itself returns after enqueueing.
+ * Host buffers should be page-locked (cudaHostAlloc / torch pin_memory) for the
+ * copies to be asynchronous and overlap; pageable memory works but serialises.
+ * The host buffers must stay valid until the stream has completed. */
+size_t whit_host_ws_bytes(int d, int64_t T, int64_t chunk, whit_dtype dtype, whit_lambda_mode lambda_mode,
+                          int nbuf);
+
+whit_status whit_run_host(const void* y, const void* w, const void* lambda, const void* grad_z, int d, int64_t T,
+                          int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode, void* z, void* grad_y,
+                          void* grad_lambda, int32_t* info, int64_t chunk, int nbuf, void* dev_buf,
+                          size_t dev_bytes, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,9 +17,11 @@ from ._lib import (  # noqa: F401
     whit_backward,
     whit_failures,
     whit_forward,
+    whit_host_ws_bytes,
+    whit_run_host,
     whit_ws_bytes,
 )
 from .autograd import WhittakerFn, smooth  # noqa: F401
 
 __all__ = ["smooth", "WhittakerFn", "Workspace", "whit_forward", "whit_backward", "whit_failures",
-           "whit_ws_bytes", "WhitError", "WHIT_F32", "WHIT_F64"]
+           "whit_ws_bytes", "whit_host_ws_bytes", "whit_run_host", "WhitError", "WHIT_F32", "WHIT_F64"]

@@ -19,12 +19,14 @@
 
 using whit::Params;
 
+#include "whit_internal.h"
+
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-whit_status fail(whit_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
-whit_status fail(whit_status s, const char* fmt, ...) {
+// Shared with the host executor (whit_host.cu); hidden from the ABI.
+whit_status whit_detail::fail(whit_status s, const char* fmt, ...) {
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -33,6 +35,10 @@ whit_status fail(whit_status s, const char* fmt, ...) {
   g_err = buf;
   return s;
 }
+
+using whit_detail::fail;
+
+namespace {
 
 // chunk length = TMA tile rows (whit::Tile<IO, d>::K)
 int chunk_k(int d) { return d <= 2 ? 16 : 8; }

@@ -219,3 +219,28 @@ def test_homo_full_size_fp32_and_fp64_check():
         assert np.max(np.abs(r64["z"][b] - o["z"].astype(float))) / ym <= 1e-10
         assert abs(r32["lambar"][b] - float(o["lambar"])) <= 1e-3 * abs(float(o["lambar"]))
         assert abs(r64["lambar"][b] - float(o["lambar"])) <= 1e-9 * abs(float(o["lambar"]))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+def test_host_executor_matches_device_path_bitwise(dtype, per_date):
+    """whit_run_host (HOST buffers, chunked 2-D copies, 3 slots, ragged last chunk) returns exactly
+    the device entry points' results: every series is an independent problem."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 300, 1000
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", dtype=dtype, seed=77)
+    dev = run_cuda(x, d, dtype)
+    h = {k: x[k].cpu().pin_memory() for k in ("y", "w", "lam", "g")}
+    z = torch.empty_like(h["y"]).pin_memory()
+    gy = torch.empty_like(h["y"]).pin_memory()
+    gl = torch.empty_like(h["lam"]).pin_memory()
+    info = torch.empty(B, dtype=torch.int32).pin_memory()
+    P.whit_run_host(h["y"], h["w"], h["lam"], h["g"], d, z, gy, gl, info, chunk=256, nbuf=3)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.double().numpy().T, dev["z"])
+    assert np.array_equal(gy.double().numpy().T, dev["ybar"])
+    gl_np = gl.double().numpy()
+    assert np.array_equal(gl_np.T if gl_np.ndim == 2 else gl_np, dev["lambar"])
+    assert np.array_equal(info.numpy(), dev["info"])
