@@ -150,6 +150,33 @@ whit_status whit_forward(const void* y, const void* w, const void* lambda, int d
 whit_status whit_backward(const void* grad_z, whit_ws* factor_ws, const void* z, void* grad_y,
                           void* grad_lambda);
 
+/* ---------------------------------------------------------------------------
+ * Multi-band pixels (NEXT-1; the paper's "batched multivariate vectors", P:28,
+ * C = 10 bands per pixel in its benchmark).  The C bands of a pixel
+ * share w and lambda, hence Omega and its factor; each band is its own
+ * right-hand side.  B counts PIXELS:
+ *   y, z, grad_z, grad_y   [C][T][B]       (band planes stacked)
+ *   w                      [T][B]           (shared)
+ *   lambda, grad_lambda    [T-d][B] or [B]  (shared; grad_lambda is summed over
+ *                                             bands, in band order, in fp64:
+ *                                             dL/dlambda_r = -sum_c (D u_c)_r (D z_c)_r)
+ * 1 <= C <= 10.  The factor is formed once per pixel per sweep (every band's
+ * warp recomputes it from the same w, lambda; band 0 stores its checkpoints),
+ * so w, lambda and factor-checkpoint bytes are amortised over C bands.  The
+ * single-band entry points above are the C = 1 case (whit_forward on a C > 1
+ * workspace is WHIT_ERR_SHAPE; whit_backward works for any C). */
+size_t whit_ws_bytes_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype, whit_lambda_mode lambda_mode);
+
+whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                                 whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes,
+                                 void* cuda_stream);
+
+whit_status whit_forward_bands(const void* y, const void* w, const void* lambda, int d, int64_t T,
+                               int64_t B, int C, void* z, whit_ws* factor_ws);
+
+whit_status whit_backward_bands(const void* grad_z, whit_ws* factor_ws, const void* z, void* grad_y,
+                                void* grad_lambda);
+
 /* SYNCHRONISES the workspace stream, then reports how many series of the
  * last forward failed (non-SPD, see "Numerical failure") in *n_failed and,
  * if host_info is non-NULL, copies info[0..B) (int32) to host_info. */

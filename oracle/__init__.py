@@ -34,6 +34,7 @@ from .whittaker import (  # noqa: F401
     forward,
     backward,
     forward_backward,
+    forward_backward_bands,
     is_spd,
 )
 from .banded import (  # noqa: F401

@@ -192,3 +192,30 @@ def is_spd(w, lam, d: int) -> bool:
         return int(np.count_nonzero(w > 0)) >= d
     ev = np.linalg.eigvalsh(omega_dense(w, lam, d, dtype=np.float64))
     return bool(ev.min() > 0)
+
+
+def forward_backward_bands(Y, w, lam, d: int, G, steps: int = 2) -> dict:
+    """C bands of one pixel sharing ``w`` and ``lam`` (the paper's multivariate batching,
+    P:28; C = 10 bands per pixel in its benchmark).
+
+    Omega = W + D^T Lambda D is common to the bands, so for each band c
+    ``z_c = Omega^{-1} W y_c`` (Eq. (3)) and ``u_c = Omega^{-1} g_c``; ``dL/dy_c = w * u_c``
+    (Eq. (5)); lambda enters every band's solve, so by the chain rule
+    ``dL/dlam_r = sum_c -(D u_c)_r (D z_c)_r`` (Eq. (4) contracted with each g_c, summed).
+    ``Y``, ``G``: (C, T).  Returns long-double arrays.
+    """
+    Om = omega_dense(w, lam, d)
+    F = _Factor(Om)
+    Y = np.atleast_2d(np.asarray(Y, dtype=np.float64))
+    G = np.atleast_2d(np.asarray(G, dtype=np.float64))
+    zs, us = [], []
+    for c in range(Y.shape[0]):
+        zs.append(F.solve(_rhs(Y[c], w), steps))
+        us.append(F.solve(G[c].astype(LD), steps))
+    Z, U = np.array(zs), np.array(us)
+    ybar = np.asarray(w, dtype=np.float64).astype(LD)[None, :] * U
+    terms = -apply_D(U, d) * apply_D(Z, d)
+    lamb = terms.sum(axis=0)
+    if np.asarray(lam).ndim == 0:
+        lamb = lamb.sum()
+    return {"z": Z, "dz": apply_D(Z, d), "u": U, "ybar": ybar, "lambar": lamb, "lambar_terms": terms}

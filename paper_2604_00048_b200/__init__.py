@@ -15,7 +15,10 @@ from ._lib import (  # noqa: F401
     WhitError,
     Workspace,
     whit_backward,
+    whit_backward_bands,
     whit_failures,
+    whit_forward_bands,
+    whit_ws_bytes_bands,
     whit_forward,
     whit_host_ws_bytes,
     whit_run_host,
@@ -24,4 +27,5 @@ from ._lib import (  # noqa: F401
 from .autograd import WhittakerFn, smooth  # noqa: F401
 
 __all__ = ["smooth", "WhittakerFn", "Workspace", "whit_forward", "whit_backward", "whit_failures",
-           "whit_ws_bytes", "whit_host_ws_bytes", "whit_run_host", "WhitError", "WHIT_F32", "WHIT_F64"]
+           "whit_ws_bytes", "whit_forward_bands", "whit_backward_bands",
+           "whit_ws_bytes_bands", "whit_host_ws_bytes", "whit_run_host", "WhitError", "WHIT_F32", "WHIT_F64"]

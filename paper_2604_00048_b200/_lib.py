@@ -38,6 +38,11 @@ SIGNATURES = [
     ("whit_backward", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("whit_failures", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int32)]),
     ("whit_info_device", _VP, [_VP]),
+    ("whit_ws_bytes_bands", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("whit_ws_create_bands", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, _VP, _SZ, _VP]),
+    ("whit_forward_bands", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, _VP, _VP]),
+    ("whit_backward_bands", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("whit_host_ws_bytes", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("whit_run_host", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                      _VP, _VP, _VP, _VP, _I64, ctypes.c_int, _VP, _SZ, _VP]),
@@ -97,19 +102,24 @@ def whit_ws_bytes(d: int, T: int, B: int, dtype: torch.dtype, per_date: bool) ->
     return int(_lib.whit_ws_bytes(d, T, B, _dtype_code(dtype), int(per_date)))
 
 
-class Workspace:
-    """Host handle (``whit_ws*``) plus the torch-owned device buffer it binds."""
+def whit_ws_bytes_bands(d: int, T: int, B: int, C: int, dtype: torch.dtype, per_date: bool) -> int:
+    return int(_lib.whit_ws_bytes_bands(d, T, B, C, _dtype_code(dtype), int(per_date)))
 
-    def __init__(self, d: int, T: int, B: int, dtype: torch.dtype, per_date: bool, device=None, stream=None):
-        nbytes = whit_ws_bytes(d, T, B, dtype, per_date)
+
+class Workspace:
+    """Host handle (``whit_ws*``) plus the torch-owned device buffer it binds (C bands per pixel)."""
+
+    def __init__(self, d: int, T: int, B: int, dtype: torch.dtype, per_date: bool, device=None, stream=None,
+                 C: int = 1):
+        nbytes = whit_ws_bytes_bands(d, T, B, C, dtype, per_date)
         if nbytes == 0:
-            raise WhitError(1, f"whit_ws_bytes(d={d}, T={T}, B={B})")
-        self.d, self.T, self.B, self.dtype, self.per_date = d, T, B, dtype, per_date
+            raise WhitError(1, f"whit_ws_bytes_bands(d={d}, T={T}, B={B}, C={C})")
+        self.d, self.T, self.B, self.C, self.dtype, self.per_date = d, T, B, C, dtype, per_date
         self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
         h = ctypes.c_void_p()
-        _check(_lib.whit_ws_create(ctypes.byref(h), d, T, B, _dtype_code(dtype), int(per_date),
-                                   ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
-               "whit_ws_create")
+        _check(_lib.whit_ws_create_bands(ctypes.byref(h), d, T, B, C, _dtype_code(dtype), int(per_date),
+                                         ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
+               "whit_ws_create_bands")
         self.handle = h
 
     def set_stream(self, stream=None):
@@ -124,6 +134,15 @@ class Workspace:
 
 def whit_forward(y, w, lam, d: int, T: int, B: int, z, ws: Workspace):
     _check(_lib.whit_forward(_ptr(y), _ptr(w), _ptr(lam), d, T, B, _ptr(z), ws.handle), "whit_forward")
+
+
+def whit_forward_bands(y, w, lam, d: int, T: int, B: int, C: int, z, ws: Workspace):
+    _check(_lib.whit_forward_bands(_ptr(y), _ptr(w), _ptr(lam), d, T, B, C, _ptr(z), ws.handle), "whit_forward_bands")
+
+
+def whit_backward_bands(grad_z, ws: Workspace, z, grad_y, grad_lambda):
+    _check(_lib.whit_backward_bands(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)),
+           "whit_backward_bands")
 
 
 def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):

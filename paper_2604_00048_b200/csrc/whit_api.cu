@@ -49,20 +49,26 @@ static_assert(whit::Tile<float, 1, false>::K == 16 && whit::Tile<float, 2, true>
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-  size_t off_dz, off_ckf, off_ckb, off_info, off_cnt, total;
+  size_t off_dz, off_ckfac, off_ckrf, off_ckrb, off_info, off_cnt, total;
 };
 
-bool layout(int d, int64_t T, int64_t B, whit_dtype dt, WsLayout* L) {
-  if (d < 1 || d > 3 || T < d + 1 || B < 1 || (dt != WHIT_F32 && dt != WHIT_F64)) return false;
+// Workspace of nb bands x B pixels: D z cache [nb][T-d][B] (I/O dtype), factor
+// checkpoints [C][NFAC][B] + forward / backward rhs checkpoints [C][nb][d][B]
+// (fp64), info[B], a failure counter.
+bool layout(int d, int64_t T, int64_t B, int nb, whit_dtype dt, WsLayout* L) {
+  if (d < 1 || d > 3 || T < d + 1 || B < 1 || nb < 1 || nb > whit::kMaxBands ||
+      (dt != WHIT_F32 && dt != WHIT_F64))
+    return false;
   const size_t esz = dt == WHIT_F32 ? 4 : 8;
   const int64_t C = (T + chunk_k(d) - 1) / chunk_k(d);
-  const int nf = d + d * (d - 1) / 2 + d;
+  const int nfac = d + d * (d - 1) / 2;
   size_t o = 0;
-  L->off_dz = o;   o = align256(o + size_t(T - d) * size_t(B) * esz);
-  L->off_ckf = o;  o = align256(o + size_t(C) * nf * size_t(B) * 8);
-  L->off_ckb = o;  o = align256(o + size_t(C) * d * size_t(B) * 8);
-  L->off_info = o; o = align256(o + size_t(B) * 4);
-  L->off_cnt = o;  o = align256(o + 8);
+  L->off_dz = o;    o = align256(o + size_t(nb) * size_t(T - d) * size_t(B) * esz);
+  L->off_ckfac = o; o = align256(o + size_t(C) * nfac * size_t(B) * 8);
+  L->off_ckrf = o;  o = align256(o + size_t(C) * nb * d * size_t(B) * 8);
+  L->off_ckrb = o;  o = align256(o + size_t(C) * nb * d * size_t(B) * 8);
+  L->off_info = o;  o = align256(o + size_t(B) * 4);
+  L->off_cnt = o;   o = align256(o + 8);
   L->total = o;
   return true;
 }
@@ -81,17 +87,19 @@ bool get_encode() {
   return g_encode != nullptr;
 }
 
-// 2-D map over a [rows][inner] plane, box {box_inner, box_rows}; out-of-bounds
-// elements (negative or >= rows, >= inner) read as zero.
-whit_status encode_map(CUtensorMap* m, const void* ptr, whit_dtype dt, int64_t inner, int64_t rows, int box_inner,
-                       int box_rows) {
+// Map over [depth][rows][inner] (depth = 0: a 2-D [rows][inner] plane), box
+// {32, box_rows(, 1)}; out-of-bounds elements (negative or >= rows, >= inner)
+// read as zero and are clipped on store.
+whit_status encode_map(CUtensorMap* m, const void* ptr, whit_dtype dt, int64_t inner, int64_t rows, int box_rows,
+                       int depth = 0) {
   if (!get_encode()) return fail(WHIT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   const size_t esz = dt == WHIT_F32 ? 4 : 8;
-  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(inner) * esz};
-  cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(m, dt == WHIT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+  const cuuint32_t rank = depth > 0 ? 3 : 2;
+  cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(depth > 0 ? depth : 1)};
+  cuuint64_t strides[2] = {cuuint64_t(inner) * esz, cuuint64_t(inner) * esz * cuuint64_t(rows)};
+  cuuint32_t box[3] = {32u, cuuint32_t(box_rows), 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, dt == WHIT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
                         const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -107,6 +115,7 @@ struct whit_ws {
   int device;  // CUDA device current at creation (-1: none), made current around encodes/launches
   int d;
   int64_t T, B;
+  int nb;      // bands per pixel sharing w, lambda (1 = independent series)
   whit_dtype dt;
   whit_lambda_mode lm;
   char* buf;
@@ -137,67 +146,75 @@ struct DeviceGuard {
   }
 };
 
-template <int D, typename IO, bool PD, bool BWD>
+template <int D, typename IO, bool PD, bool BWD, bool MB>
 whit_status launch(const Params& p, cudaStream_t s) {
   using L = whit::Layout<D, IO, PD, BWD>;
+  constexpr int max_smem = MB ? L::smem_mb(whit::kMaxBands) : L::SMEM;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    L::SMEM);
+    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
   });
   if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  constexpr int per_cta = 32 * L::WARPS;  // one series per thread, one TMA pipeline per warp
+  // one pixel per thread, one TMA pipeline per warp
+  const int threads = MB ? 32 * p.nb : 32 * L::WARPS;
+  const long long per_cta = MB ? 32 : threads;
   const long long grid = (p.B + per_cta - 1) / per_cta;
-  whit::whit_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(per_cta), L::SMEM, s>>>(p);
+  const int smem = MB ? L::smem_mb(p.nb) : L::SMEM;
+  whit::whit_kernel<D, IO, PD, BWD, MB><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
 }
 
-template <typename IO, bool PD, bool BWD>
+template <typename IO, bool PD, bool BWD, bool MB>
 whit_status dispatch_d(int d, const Params& p, cudaStream_t s) {
   switch (d) {
-    case 1: return launch<1, IO, PD, BWD>(p, s);
-    case 2: return launch<2, IO, PD, BWD>(p, s);
-    case 3: return launch<3, IO, PD, BWD>(p, s);
+    case 1: return launch<1, IO, PD, BWD, MB>(p, s);
+    case 2: return launch<2, IO, PD, BWD, MB>(p, s);
+    case 3: return launch<3, IO, PD, BWD, MB>(p, s);
   }
   return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
 }
 
-template <bool BWD>
-whit_status dispatch(const whit_ws* ws, const Params& p) {
-  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
-  if (ws->dt == WHIT_F32)
-    return pd ? dispatch_d<float, true, BWD>(ws->d, p, ws->stream) : dispatch_d<float, false, BWD>(ws->d, p, ws->stream);
-  return pd ? dispatch_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_d<double, false, BWD>(ws->d, p, ws->stream);
+template <typename IO, bool BWD, bool MB>
+whit_status dispatch_pd(const whit_ws* ws, const Params& p) {
+  return ws->lm == WHIT_LAMBDA_PER_DATE ? dispatch_d<IO, true, BWD, MB>(ws->d, p, ws->stream)
+                                        : dispatch_d<IO, false, BWD, MB>(ws->d, p, ws->stream);
 }
 
-// TMA box inner extent: one warp's 32 series.
-int tile_nt(whit_dtype) { return 32; }
+template <bool BWD>
+whit_status dispatch(const whit_ws* ws, const Params& p) {
+  const bool mb = ws->nb > 1;
+  if (ws->dt == WHIT_F32)
+    return mb ? dispatch_pd<float, BWD, true>(ws, p) : dispatch_pd<float, BWD, false>(ws, p);
+  return mb ? dispatch_pd<double, BWD, true>(ws, p) : dispatch_pd<double, BWD, false>(ws, p);
+}
 
 // Fill the tensor maps and plain pointers common to both directions.
 whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const void* w, const void* lam) {
   std::memset(p, 0, sizeof *p);
-  const int nt = tile_nt(ws->dt);
   const int d = ws->d;
   const int kK = chunk_k(d);
   whit_status st;
-  if ((st = encode_map(&p->tm_rhs, rhs, ws->dt, ws->B, ws->T, nt, kK)) != WHIT_OK) return st;
-  if ((st = encode_map(&p->tm_w, w, ws->dt, ws->B, ws->T, nt, kK)) != WHIT_OK) return st;
+  if ((st = encode_map(&p->tm_rhs, rhs, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
+  if ((st = encode_map(&p->tm_w, w, ws->dt, ws->B, ws->T, kK)) != WHIT_OK) return st;
   if (ws->lm == WHIT_LAMBDA_PER_DATE) {
-    if ((st = encode_map(&p->tm_lam_up, lam, ws->dt, ws->B, ws->T - d, nt, kK)) != WHIT_OK) return st;
-    if ((st = encode_map(&p->tm_lam_dn, lam, ws->dt, ws->B, ws->T - d, nt, kK + d)) != WHIT_OK) return st;
+    if ((st = encode_map(&p->tm_lam_up, lam, ws->dt, ws->B, ws->T - d, kK)) != WHIT_OK) return st;
+    if ((st = encode_map(&p->tm_lam_dn, lam, ws->dt, ws->B, ws->T - d, kK + d)) != WHIT_OK) return st;
     p->lam_plane = lam;
   } else {
     p->lam_scalar = lam;
   }
-  p->ck_f = reinterpret_cast<double*>(ws->buf + ws->L.off_ckf);
-  p->ck_b = reinterpret_cast<double*>(ws->buf + ws->L.off_ckb);
+  p->ck_fac = reinterpret_cast<double*>(ws->buf + ws->L.off_ckfac);
+  p->ck_rhs_f = reinterpret_cast<double*>(ws->buf + ws->L.off_ckrf);
+  p->ck_rhs_b = reinterpret_cast<double*>(ws->buf + ws->L.off_ckrb);
   p->info = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_info);
   p->B = ws->B;
   p->T = int(ws->T);
   p->C = int((ws->T + kK - 1) / kK);
+  p->nb = ws->nb;
   return WHIT_OK;
 }
 
@@ -222,18 +239,23 @@ const char* whit_status_string(whit_status s) {
 
 const char* whit_last_error(void) { return g_err.c_str(); }
 
-size_t whit_ws_bytes(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode) {
+size_t whit_ws_bytes_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype, whit_lambda_mode lambda_mode) {
   WsLayout L;
   if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE) return 0;
-  if (!layout(d, T, B, dtype, &L)) return 0;
+  if (!layout(d, T, B, C, dtype, &L)) return 0;
   return L.total;
 }
 
-whit_status whit_ws_create(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
-                           whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream) {
+size_t whit_ws_bytes(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode) {
+  return whit_ws_bytes_bands(d, T, B, 1, dtype, lambda_mode);
+}
+
+whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                                 whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream) {
   if (!out) return fail(WHIT_ERR_ARG, "out is NULL");
   *out = nullptr;
   if (d < 1 || d > 3) return fail(WHIT_ERR_ARG, "d = %d not in {1,2,3}", d);
+  if (C < 1 || C > whit::kMaxBands) return fail(WHIT_ERR_ARG, "bands C = %d not in [1, %d]", C, whit::kMaxBands);
   if (dtype != WHIT_F32 && dtype != WHIT_F64) return fail(WHIT_ERR_ARG, "bad dtype %d", int(dtype));
   if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE)
     return fail(WHIT_ERR_ARG, "bad lambda mode %d", int(lambda_mode));
@@ -244,14 +266,14 @@ whit_status whit_ws_create(whit_ws** out, int d, int64_t T, int64_t B, whit_dtyp
     return fail(WHIT_ERR_ALIGN, "B = %lld must be a multiple of %d (16-B row stride)", (long long)B,
                 dtype == WHIT_F32 ? 4 : 2);
   WsLayout L;
-  layout(d, T, B, dtype, &L);
+  layout(d, T, B, C, dtype, &L);
   if (!dev_buf) return fail(WHIT_ERR_WS, "workspace buffer is NULL");
   if (reinterpret_cast<uintptr_t>(dev_buf) & 255u) return fail(WHIT_ERR_ALIGN, "workspace buffer not 256-B aligned");
   if (dev_bytes < L.total)
     return fail(WHIT_ERR_WS, "workspace %zu bytes < required %zu", dev_bytes, L.total);
   whit_ws* ws = new (std::nothrow) whit_ws;
   if (!ws) return fail(WHIT_ERR_ARG, "host allocation failed");
-  ws->d = d; ws->T = T; ws->B = B; ws->dt = dtype; ws->lm = lambda_mode;
+  ws->d = d; ws->T = T; ws->B = B; ws->nb = C; ws->dt = dtype; ws->lm = lambda_mode;
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
@@ -264,6 +286,11 @@ whit_status whit_ws_create(whit_ws** out, int d, int64_t T, int64_t B, whit_dtyp
   return WHIT_OK;
 }
 
+whit_status whit_ws_create(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
+                           whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream) {
+  return whit_ws_create_bands(out, d, T, B, 1, dtype, lambda_mode, dev_buf, dev_bytes, cuda_stream);
+}
+
 whit_status whit_ws_set_stream(whit_ws* ws, void* cuda_stream) {
   if (!ws) return fail(WHIT_ERR_ARG, "ws is NULL");
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -272,13 +299,13 @@ whit_status whit_ws_set_stream(whit_ws* ws, void* cuda_stream) {
 
 void whit_ws_destroy(whit_ws* ws) { delete ws; }
 
-whit_status whit_forward(const void* y, const void* w, const void* lambda, int d, int64_t T, int64_t B, void* z,
-                         whit_ws* ws) {
+whit_status whit_forward_bands(const void* y, const void* w, const void* lambda, int d, int64_t T, int64_t B, int C,
+                               void* z, whit_ws* ws) {
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!y || !w || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
-  if (d != ws->d || T != ws->T || B != ws->B)
-    return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
-                (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
+  if (d != ws->d || T != ws->T || B != ws->B || C != ws->nb)
+    return fail(WHIT_ERR_SHAPE, "(d,T,B,C) = (%d,%lld,%lld,%d) != workspace (%d,%lld,%lld,%d)", d, (long long)T,
+                (long long)B, C, ws->d, (long long)ws->T, (long long)ws->B, ws->nb);
   if (!aligned16(y) || !aligned16(w) || !aligned16(lambda) || !aligned16(z))
     return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
   if (z == y || z == w || z == lambda) return fail(WHIT_ERR_ARG, "z aliases an input");
@@ -287,17 +314,21 @@ whit_status whit_forward(const void* y, const void* w, const void* lambda, int d
   Params p;
   whit_status st = fill_params(ws, &p, y, w, lambda);
   if (st != WHIT_OK) return st;
-  p.out0 = z;
-  p.out1 = ws->buf + ws->L.off_dz;
   const int kK = chunk_k(d);
-  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, tile_nt(ws->dt), kK)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out1, p.out1, ws->dt, B, T - d, tile_nt(ws->dt), kK)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
   ws->have_fwd = false;
   st = dispatch<false>(ws, p);
   if (st != WHIT_OK) return st;
   ws->have_fwd = true;
   ws->w = w; ws->lam = lambda; ws->z = z;
   return WHIT_OK;
+}
+
+whit_status whit_forward(const void* y, const void* w, const void* lambda, int d, int64_t T, int64_t B, void* z,
+                         whit_ws* ws) {
+  if (ws && ws->nb != 1) return fail(WHIT_ERR_SHAPE, "workspace has %d bands: use whit_forward_bands", ws->nb);
+  return whit_forward_bands(y, w, lambda, d, T, B, 1, z, ws);
 }
 
 whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* grad_y, void* grad_lambda) {
@@ -314,17 +345,20 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
   Params p;
   whit_status st = fill_params(ws, &p, grad_z, ws->w, ws->lam);
   if (st != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_dz, ws->buf + ws->L.off_dz, ws->dt, ws->B, ws->T - ws->d, tile_nt(ws->dt),
-                      chunk_k(ws->d))) != WHIT_OK)
-    return st;
-  p.out0 = grad_y;
-  p.out1 = grad_lambda;
   const int kK = chunk_k(ws->d);
-  if ((st = encode_map(&p.tm_out0, grad_y, ws->dt, ws->B, ws->T, tile_nt(ws->dt), kK)) != WHIT_OK) return st;
-  if (ws->lm == WHIT_LAMBDA_PER_DATE &&
-      (st = encode_map(&p.tm_out1, grad_lambda, ws->dt, ws->B, ws->T - ws->d, tile_nt(ws->dt), kK)) != WHIT_OK)
+  if ((st = encode_map(&p.tm_dz, ws->buf + ws->L.off_dz, ws->dt, ws->B, ws->T - ws->d, kK, ws->nb)) != WHIT_OK)
     return st;
+  if ((st = encode_map(&p.tm_out0, grad_y, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
+  if (ws->lm == WHIT_LAMBDA_PER_DATE) {
+    if ((st = encode_map(&p.tm_out1, grad_lambda, ws->dt, ws->B, ws->T - ws->d, kK)) != WHIT_OK) return st;
+  } else {
+    p.out1 = grad_lambda;
+  }
   return dispatch<true>(ws, p);
+}
+
+whit_status whit_backward_bands(const void* grad_z, whit_ws* ws, const void* z, void* grad_y, void* grad_lambda) {
+  return whit_backward(grad_z, ws, z, grad_y, grad_lambda);
 }
 
 whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {

@@ -44,24 +44,28 @@ __host__ __device__ __forceinline__ constexpr double Cj(int d, int j) {
 }
 
 // ------------------------------------------------------------------ kernel parameters
+// B = number of pixels; nb = bands per pixel sharing w, lambda and therefore
+// Omega (NEXT-1; nb = 1: independent series).  Band planes are
+// [nb][rows][B] and use 3-D maps {B, rows, nb}; w and lambda are 2-D [rows][B].
 struct Params {
-  CUtensorMap tm_rhs;     // y (forward) or grad_z (backward): [T][B], box {32, K}
+  CUtensorMap tm_rhs;     // y (forward) or grad_z (backward): [nb][T][B], box {32, K, 1}
   CUtensorMap tm_w;       // w: [T][B], box {32, K}
   CUtensorMap tm_lam_up;  // per-date lambda [T-d][B], box {32, K}
   CUtensorMap tm_lam_dn;  // per-date lambda [T-d][B], box {32, K+d} (rows t0-d..t0+K-1)
-  CUtensorMap tm_dz;      // D z cache [T-d][B], box {32, K} (backward only)
-  CUtensorMap tm_out0;    // z (forward) / grad_y (backward): [T][B], box {32, K}  (TMA store)
-  CUtensorMap tm_out1;    // D z (forward) / per-date grad_lambda (backward): [T-d][B], box {32, K}
+  CUtensorMap tm_dz;      // D z cache [nb][T-d][B], box {32, K, 1} (backward only)
+  CUtensorMap tm_out0;    // z (forward) / grad_y (backward): [nb][T][B], box {32, K, 1}  (TMA store)
+  CUtensorMap tm_out1;    // forward: D z cache [nb][T-d][B] (3-D); backward: per-date grad_lambda [T-d][B] (2-D)
   const void* lam_scalar; // [B] (scalar lambda mode)
   const void* lam_plane;  // [T-d][B] (per-date mode; read directly only by the cold failure path)
-  void* out0;             // forward: z [T][B]; backward: grad_y [T][B]
-  void* out1;             // forward: D z [T-d][B] (ws); backward: grad_lambda
-  double* ck_f;           // forward checkpoints [C][NF][B]  (factor + rhs state)
-  double* ck_b;           // backward checkpoints [C][d][B]  (rhs state)
+  void* out1;             // backward, scalar lambda: grad_lambda [B]
+  double* ck_fac;         // factor checkpoints [C][NFAC][B] (written by band 0, read by all bands)
+  double* ck_rhs_f;       // forward rhs checkpoints [C][nb][d][B]
+  double* ck_rhs_b;       // backward rhs checkpoints [C][nb][d][B]
   int32_t* info;          // [B]
   long long B;
   int T;
   int C;                  // number of K-step chunks = ceil(T / K)
+  int nb;                 // bands per pixel
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -97,6 +101,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
@@ -244,12 +260,16 @@ template <int D> struct Ck {
 // Registers are allocated per pair of warps.  Forward: 4-warp CTAs, 3 per SM
 // (12 warps, <= 168 regs, 16.8 KB smem per warp).  Backward (one more staged
 // input plane, 21 KB per warp): 2-warp CTAs, 5 per SM (10 warps, <= 200 regs).
+// Multi-band (MB): one CTA = nb warps (one band each) over the same 32 pixels,
+// at most 10 warps (<= 200 regs) per SM.
 template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int K = D <= 2 ? 16 : 8;
   static constexpr int ST = 2;
   static constexpr int WARPS = BWD ? 2 : 4;
   static constexpr int MAXREG = BWD ? 200 : 168;
+  static constexpr int MB_MAXREG = 200;
 };
+constexpr int kMaxBands = 10;
 
 template <int D, typename IO, bool PD, bool BWD> struct Layout {
   static constexpr int K = Tile<IO, D, BWD>::K, ST = Tile<IO, D, BWD>::ST, WARPS = Tile<IO, D, BWD>::WARPS;
@@ -262,6 +282,8 @@ template <int D, typename IO, bool PD, bool BWD> struct Layout {
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
   static constexpr int WARP_SMEM = ST * STAGE + 2 * OUT;     // ring + out0 + out1
   static constexpr int SMEM = WARPS * WARP_SMEM;
+  // multi-band CTA of nb warps: rings + reduction tile + scalar slots
+  static constexpr int smem_mb(int nb) { return nb * WARP_SMEM + OUT + nb * 32 * 8; }
   static constexpr uint32_t BYTES_UP = (2 * K + (PD ? K : 0)) * ROW;
   static constexpr uint32_t BYTES_DN = (2 * K + (PD ? K + D : 0) + (BWD ? K : 0)) * ROW;
 };
@@ -269,19 +291,19 @@ template <int D, typename IO, bool PD, bool BWD> struct Layout {
 // Issue tile i (up sweep tiles 0..C-1, then down sweep C-1..0) of one warp.
 template <int D, typename IO, bool PD, bool BWD>
 __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage, uint64_t* bar, int i, int C,
-                                           int c0) {
+                                           int c0, int band) {
   using L = Layout<D, IO, PD, BWD>;
   const bool up = i < C;
   const int c = up ? i : 2 * C - 1 - i;
   const int t0 = c * L::K;
   mbar_arrive_expect_tx(bar, up ? L::BYTES_UP : L::BYTES_DN);
-  tma_load_2d(stage + L::OFF_RHS, &p.tm_rhs, c0, t0, bar);
+  tma_load_3d(stage + L::OFF_RHS, &p.tm_rhs, c0, t0, band, bar);
   tma_load_2d(stage + L::OFF_W, &p.tm_w, c0, t0, bar);
   if (PD) {
     if (up) tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_up, c0, t0, bar);
     else tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_dn, c0, t0 - D, bar);
   }
-  if (BWD && !up) tma_load_2d(stage + L::OFF_DZ, &p.tm_dz, c0, t0, bar);
+  if (BWD && !up) tma_load_3d(stage + L::OFF_DZ, &p.tm_dz, c0, t0, band, bar);
 }
 
 // ------------------------------------------------------------------ per-thread sweep bodies
@@ -322,17 +344,16 @@ struct Sweep {
   // restore of the down sweep and the same ldl_step (bitwise-identical).
   static __device__ __noinline__ int first_bad_row(const Params& p, int c, long long b, const unsigned char* stg,
                                                    int lane, int t0, int T, double lam_s) {
-    constexpr int NF = Ck<D>::NF;
+    constexpr int NFAC = Ck<D>::NFAC;
     const long long B = p.B;
-    const double* ck = p.ck_f + (long long)c * NF * B + b;
+    const double* ck = p.ck_fac + (long long)c * NFAC * B + b;
     const IO* lam_plane = reinterpret_cast<const IO*>(p.lam_plane);
     FState<D> st;
-    state_init<D>(st);
+    state_init<D>(st);  // v = 0: the pivots do not depend on the right-hand side
     int f = 0;
     for (int i = 0; i < D; ++i) st.dl[i] = ck[(long long)(f++) * B];
     for (int m = 0; m < D - 1; ++m)
       for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = ck[(long long)(f++) * B];
-    for (int i = 0; i < D; ++i) st.v[i] = ck[(long long)(f++) * B];
     for (int i = 0; i < D; ++i) {
       const int tj = t0 - 1 - i;
       const bool in = tj >= 0 && tj < T - D;
@@ -432,22 +453,29 @@ struct Sweep {
 
 // ------------------------------------------------------------------ the kernel
 // One launch = one full forward (BWD=false) or backward (BWD=true).  Each
-// warp owns 32 consecutive series and its own TMA ring: up sweep over C
-// chunks, then down sweep over C chunks in reverse.
-template <int D, typename IO, bool PD, bool BWD>
-__global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid_constant__ Params p) {
+// warp owns 32 consecutive pixels x one band and its own TMA ring: up sweep
+// over C chunks, then down sweep over C chunks in reverse.
+//   MB = false: independent series (nb = 1), WARPS independent warps per CTA.
+//   MB = true : CTA = nb warps, one per band of the same 32 pixels; they share
+//               the factor (band 0 writes its checkpoints, every band reads
+//               them) and, in the backward, reduce -(Du_c)(Dz_c) over bands in
+//               shared memory in band order (deterministic).
+template <int D, typename IO, bool PD, bool BWD, bool MB>
+__global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>::MAXREG))
+    whit_kernel(const __grid_constant__ Params p) {
   using L = Layout<D, IO, PD, BWD>;
   using S = Sweep<D, IO, PD, BWD>;
-  constexpr int K = L::K, ST = L::ST, WARPS = L::WARPS;
-  constexpr int NF = Ck<D>::NF, NFAC = Ck<D>::NFAC;
+  constexpr int K = L::K, ST = L::ST;
+  constexpr int NFAC = Ck<D>::NFAC;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[WARPS][ST];
+  __shared__ __align__(8) uint64_t full_bar[MB ? kMaxBands : L::WARPS][ST];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = p.T, C = p.C;
+  const int T = p.T, C = p.C, nb = MB ? p.nb : 1;
   const long long B = p.B;
-  const long long bw = ((long long)blockIdx.x * WARPS + warp) * 32;  // this warp's first series
-  if (bw >= B) return;  // whole warp past the end (no CTA-wide barrier follows)
+  const int band = MB ? warp : 0;
+  const long long bw = MB ? (long long)blockIdx.x * 32 : ((long long)blockIdx.x * L::WARPS + warp) * 32;
+  if (bw >= B) return;  // (MB: the whole CTA) past the end; no barrier follows for these warps
   const long long b = bw + lane;
   const bool valid = b < B;
   unsigned char* ring = smem + warp * L::WARP_SMEM;
@@ -455,18 +483,23 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
   IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
   uint64_t* bars = full_bar[warp];
   const int ntiles = 2 * C;
+  // MB backward: per-CTA reduction tile (K rows x 32 pixels) and scalar slots
+  IO* red = reinterpret_cast<IO*>(smem + (MB ? nb : 0) * L::WARP_SMEM);
+  double* redS = reinterpret_cast<double*>(smem + (MB ? nb : 0) * L::WARP_SMEM + L::OUT);
 
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < ST && i < ntiles; ++i)
-      issue_tile<D, IO, PD, BWD>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw);
+      issue_tile<D, IO, PD, BWD>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw, band);
   }
   __syncwarp();
 
   const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
   const int cr = (T - D) / K;  // first chunk that reaches row T-D (ragged handling from there on)
+  double* const ck_rhs = (BWD ? p.ck_rhs_b : p.ck_rhs_f) + (long long)band * D * B + b;  // + c * nb * D * B
+  const long long ck_rhs_stride = (long long)nb * D * B;
 
   FState<D> st;
   state_init<D>(st);
@@ -480,8 +513,8 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
     const unsigned char* stg = ring + s * L::STAGE;
     const int t0 = c * K;
     if (valid) {  // checkpoint: state entering row t0
-      if (!BWD) {
-        double* ck = p.ck_f + (long long)c * NF * B + b;
+      if (!BWD && band == 0) {
+        double* ck = p.ck_fac + (long long)c * NFAC * B + b;
         int f = 0;
 #pragma unroll
         for (int i = 0; i < D; ++i) ck[(long long)(f++) * B] = st.dl[i];
@@ -489,13 +522,10 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
         for (int m = 0; m < D - 1; ++m)
 #pragma unroll
           for (int k = 0; k < D - 1 - m; ++k) ck[(long long)(f++) * B] = st.ap[m][k];
-#pragma unroll
-        for (int i = 0; i < D; ++i) ck[(long long)(f++) * B] = st.v[i];
-      } else {
-        double* ck = p.ck_b + (long long)c * D * B + b;
-#pragma unroll
-        for (int i = 0; i < D; ++i) ck[(long long)i * B] = st.v[i];
       }
+      double* ck = ck_rhs + (long long)c * ck_rhs_stride;
+#pragma unroll
+      for (int i = 0; i < D; ++i) ck[(long long)i * B] = st.v[i];
     }
     bool pos = true;
     if (c < cr) S::template up_chunk<false>(st, stg, lane, t0, T, lam_s, nobs, pos);
@@ -504,7 +534,7 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw);
+      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }
   }
 
@@ -512,10 +542,11 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
   // singular for lambda > 0); else first non-positive pivot row.  A failed
   // series is poisoned with NaN in the restored rhs state, so every output
   // derived from it (z, D z, w*u, -(D u)(D z)) is NaN without per-store checks.
+  // All bands of a pixel compute the identical factor, hence the same status.
   bool failed;
   if (!BWD) {
     const int info = (nobs < D) ? (T - D + 1) : bad;
-    if (valid) p.info[b] = info;
+    if (valid && band == 0) p.info[b] = info;
     failed = info != 0;
   } else {
     failed = valid ? (p.info[b] != 0) : true;
@@ -538,15 +569,11 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
 #define WHIT_LOAD_CK(cc)                                                                          \
   do {                                                                                            \
     if (valid) {                                                                                  \
-      const double* ckf = p.ck_f + (long long)(cc) * NF * B + b;                                  \
+      const double* ckf = p.ck_fac + (long long)(cc) * NFAC * B + b;                              \
       _Pragma("unroll") for (int i = 0; i < D; ++i) pdl[i] = ckf[(long long)i * B];               \
       _Pragma("unroll") for (int f = 0; f < NFAC - D; ++f) pap[f] = ckf[(long long)(D + f) * B];  \
-      if (!BWD) {                                                                                 \
-        _Pragma("unroll") for (int i = 0; i < D; ++i) pv[i] = ckf[(long long)(NFAC + i) * B];     \
-      } else {                                                                                    \
-        const double* ckb = p.ck_b + (long long)(cc) * D * B + b;                                 \
-        _Pragma("unroll") for (int i = 0; i < D; ++i) pv[i] = ckb[(long long)i * B];              \
-      }                                                                                           \
+      const double* ckr = ck_rhs + (long long)(cc) * ck_rhs_stride;                               \
+      _Pragma("unroll") for (int i = 0; i < D; ++i) pv[i] = ckr[(long long)i * B];                \
     }                                                                                             \
   } while (0)
   WHIT_LOAD_CK(C - 1);
@@ -587,18 +614,50 @@ __global__ void __maxnreg__((Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
     if (lane == 0) {
-      tma_store_2d(&p.tm_out0, so0, (int)bw, t0);
-      if (!BWD || PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
+      tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
+      if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
+      if (BWD && PD && !MB) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
       bulk_commit();
     }
+    if (MB && BWD && PD) {
+      // grad_lambda_r = sum over bands of -(D u_c)_r (D z_c)_r, summed in band order in fp64
+      if (threadIdx.x == 0) bulk_wait_read0();  // previous reduced tile has been read by its store
+      __syncthreads();
+      for (int k = warp; k < K; k += nb) {
+        double acc = 0.0;
+        for (int cb = 0; cb < nb; ++cb)
+          acc += to_f64<IO>(reinterpret_cast<const IO*>(smem + cb * L::WARP_SMEM + ST * L::STAGE + L::OUT)[k * 32 + lane]);
+        red[k * 32 + lane] = from_f64<IO>(acc);
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma_store_2d(&p.tm_out1, red, (int)bw, t0);
+        bulk_commit();
+      }
+    }
+
+    __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw);
+      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }
   }
 #undef WHIT_LOAD_CK
   if (lane == 0) bulk_wait0();  // stores complete before the CTA exits (smem stays valid)
-  if (BWD && !PD && valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc);
+  if (BWD && !PD) {
+    if (MB) {  // scalar lambda: reduce the per-band sums in band order
+      redS[warp * 32 + lane] = lam_acc;
+      __syncthreads();
+      if (warp == 0) {
+        double acc = 0.0;
+        for (int cb = 0; cb < nb; ++cb) acc += redS[cb * 32 + lane];
+        if (valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(acc);
+      }
+    } else if (valid) {
+      reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc);
+    }
+  }
 }
 
 // Count of failed series (info != 0) for whit_failures.

@@ -212,3 +212,34 @@ def series_major(x: torch.Tensor):
     import numpy as np
     a = x.detach().to("cpu", torch.float64).numpy()
     return np.ascontiguousarray(a.T) if a.ndim == 2 else a
+
+
+def make_inputs_bands(cfg: Config | str, C: int, *, B: int | None = None, T: int | None = None,
+                      d: int | None = None, seed: int | None = None, series_offset: int = 0, device="cpu",
+                      dtype=torch.float32, lam_mode: str | None = None, mask: str | None = None,
+                      row_chunk_elems: int = 1 << 24) -> dict:
+    """C reflectance bands per pixel sharing the mask and lambda (BASELINE 's2tile' shape):
+    band c = a_c (ndvi - 0.45) / 0.2 + b_c + 0.1 N(0, 1) (standardised-reflectance-like),
+    a_c in [-1, 1], b_c in [-0.5, 0.5] fixed per band.  Returns y, g as [C][T][B]; w [T][B];
+    lam [T-d][B] or [B]."""
+    base = make_inputs(cfg, B=B, T=T, d=d, seed=seed, series_offset=series_offset, device=device,
+                       dtype=torch.float64, lam_mode=lam_mode, mask=mask, row_chunk_elems=row_chunk_elems)
+    T, B, d = base["T"], base["B"], base["d"]
+    dev = torch.device(device)
+    ser = torch.arange(series_offset, series_offset + B, dtype=torch.int64, device=dev)
+    S = _Stream(base["seed"], ser)
+    y = torch.empty((C, T, B), dtype=dtype, device=dev)
+    g = torch.empty((C, T, B), dtype=dtype, device=dev)
+    R = max(1, row_chunk_elems // max(B, 1))
+    for c in range(C):
+        kc = _uniform(_key(base["seed"], 900 + c)).item()
+        a_c = -1.0 + 2.0 * kc
+        b_c = -0.5 + _uniform(_key(base["seed"], 950 + c)).item()
+        for t0 in range(0, T, R):
+            t1 = min(T, t0 + R)
+            t = torch.arange(t0, t1, dtype=torch.int64, device=dev)[:, None]
+            nz = _normal(S.per_cell(100 + 4 * c, t), S.per_cell(101 + 4 * c, t))
+            y[c, t0:t1] = (a_c * (base["y"][t0:t1] - 0.45) / 0.2 + b_c + 0.1 * nz).to(dtype)
+            g[c, t0:t1] = _normal(S.per_cell(102 + 4 * c, t), S.per_cell(103 + 4 * c, t)).to(dtype)
+    return {"y": y, "w": base["w"].to(dtype), "lam": base["lam"].to(dtype), "g": g, "B": B, "T": T, "d": d, "C": C,
+            "lam_mode": base["lam_mode"], "seed": base["seed"], "series_offset": series_offset}

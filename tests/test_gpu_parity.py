@@ -244,3 +244,63 @@ def test_host_executor_matches_device_path_bitwise(dtype, per_date):
     gl_np = gl.double().numpy()
     assert np.array_equal(gl_np.T if gl_np.ndim == 2 else gl_np, dev["lambar"])
     assert np.array_equal(info.numpy(), dev["info"])
+
+
+def run_cuda_bands(x: dict, d: int, C: int, dtype):
+    import paper_2604_00048_b200 as P
+
+    y, w, lam, g = (x[k].to(dtype).contiguous() for k in ("y", "w", "lam", "g"))
+    _, T, B = y.shape
+    ws = P.Workspace(d, T, B, dtype, lam.dim() == 2, C=C)
+    z, gy, gl = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam)
+    P.whit_forward_bands(y, w, lam, d, T, B, C, z, ws)
+    P.whit_backward_bands(g, ws, z, gy, gl)
+    nfail, info = P.whit_failures(ws, with_info=True)
+    torch.cuda.synchronize()
+    return {"z": z.double().cpu().numpy(), "ybar": gy.double().cpu().numpy(), "lambar": gl.double().cpu().numpy(),
+            "nfail": nfail, "info": info}
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d,C", [(2, 10), (2, 3), (1, 4), (3, 2)])
+def test_bands_shared_factor(d, C, per_date, dtype):
+    """NEXT-1: C bands per pixel sharing w and lambda; per band vs O2 (band-series with the pixel's
+    w, lambda), lambda gradient = sum over bands (oracle O1 forward_backward_bands on a subsample)."""
+    T, B = 203, 300
+    x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                                device="cuda", dtype=dtype, seed=500 + d * 10 + C)
+    res = run_cuda_bands(x, d, C, dtype)
+    assert res["nfail"] == 0
+    tz, tg = TOL[(dtype, d)]
+    w = x["w"].double().cpu().numpy().T
+    lam = x["lam"].double().cpu().numpy()
+    lam = lam.T if lam.ndim == 2 else lam
+    for c in range(C):
+        hc = {"y": x["y"][c].double().cpu().numpy().T, "w": w, "lam": lam, "g": x["g"][c].double().cpu().numpy().T}
+        ref = O2.forward_banded(hc["y"], w, lam, d)[0]
+        ez = rel_series(res["z"][c].T, ref, ymax_observed(hc["y"], w))
+        assert ez.max() <= tz, (c, ez.max())
+        yb, _ = O2.backward_banded(hc["g"], w, lam, d, ref)
+        assert rel_series(res["ybar"][c].T, yb).max() <= tg
+    for b in (0, 137, B - 1):
+        Y = x["y"][:, :, b].double().cpu().numpy()
+        G = x["g"][:, :, b].double().cpu().numpy()
+        o = O1.forward_backward_bands(Y, w[b], lam[b] if lam.ndim == 2 else lam[b], d, G)
+        got = res["lambar"][:, b] if per_date else res["lambar"][b]
+        if per_date:
+            assert rel_series(got, o["lambar"]).max() <= tg, b
+        else:
+            den = np.sum(np.abs(o["lambar_terms"].astype(float)))
+            assert abs(got - float(o["lambar"])) / den <= tg, b
+
+
+def test_bands_one_equals_single_series_path():
+    """C = 1 through the band entry points reproduces whit_forward/whit_backward bitwise."""
+    d, T, B = 2, 150, 256
+    x = synth.make_inputs_bands("hetero", 1, B=B, T=T, d=d, device="cuda", seed=9)
+    a = run_cuda_bands(x, d, 1, torch.float32)
+    xs = {"y": x["y"][0], "w": x["w"], "lam": x["lam"], "g": x["g"][0]}
+    b = run_cuda(xs, d, torch.float32)
+    assert np.array_equal(a["z"][0].T, b["z"]) and np.array_equal(a["ybar"][0].T, b["ybar"])
+    assert np.array_equal(a["lambar"].T, b["lambar"])

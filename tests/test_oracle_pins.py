@@ -462,3 +462,30 @@ def test_O2_matches_O1_sentinel2_daily():
         assert np.max(np.abs(z2[b] - o["z"])) / np.max(np.abs(y[b])) < 1e-11
         assert rel(yb2[b], o["ybar"]) < 1e-10
         assert rel(lb2[b], o["lambar"]) < 1e-10
+
+
+# ----------------------------------------------------------------- multi-band (NEXT-1)
+@pytest.mark.parametrize("per_date", [True, False])
+def test_bands_shared_factor_fd_and_per_band(per_date):
+    """C bands sharing w, lambda: each band equals the single-band solve, and the summed
+    lambda gradient matches central finite differences of L = sum_c g_c . z_c."""
+    T, d, C = 30, 2, 3
+    Y = rng.normal(size=(C, T))
+    G = rng.normal(size=(C, T))
+    w = (rng.random(T) < 0.6).astype(float)
+    w[:3] = 1
+    lam = 10 ** rng.uniform(0, 2, T - d) if per_date else 10 ** rng.uniform(0, 2)
+    o = O1.forward_backward_bands(Y, w, lam, d, G)
+    for c in range(C):
+        s1 = O1.forward_backward(Y[c], w, lam, d, G[c])
+        assert rel(o["z"][c], s1["z"]) < 1e-15 and rel(o["ybar"][c], s1["ybar"]) < 1e-15
+
+    def L(lv):
+        return sum(float(np.dot(G[c], O1.forward(Y[c], w, lv, d)[0].astype(float))) for c in range(C))
+
+    h = 1e-6
+    if per_date:
+        fd = np.array([(L(lam * np.exp(h * e)) - L(lam * np.exp(-h * e))) / (2 * h) for e in np.eye(T - d)]) / lam
+    else:
+        fd = (L(lam * np.exp(h)) - L(lam * np.exp(-h))) / (2 * h) / lam
+    assert rel(o["lambar"], fd) < 1e-6
