@@ -160,7 +160,8 @@ whit_status whit_backward(const void* grad_z, whit_ws* factor_ws, const void* z,
  *   lambda, grad_lambda    [T-d][B] or [B]  (shared; grad_lambda is summed over
  *                                             bands, in band order, in fp64:
  *                                             dL/dlambda_r = -sum_c (D u_c)_r (D z_c)_r)
- * 1 <= C <= 10.  The factor is formed once per pixel per sweep (every band's
+ * 1 <= C <= 10 for F32 planes, <= 5 for F64 (one CTA's shared memory holds the
+ * C band pipelines).  The factor is formed once per pixel per sweep (every band's
  * warp recomputes it from the same w, lambda; band 0 stores its checkpoints),
  * so w, lambda and factor-checkpoint bytes are amortised over C bands.  The
  * single-band entry points above are the C = 1 case (whit_forward on a C > 1

@@ -146,10 +146,29 @@ struct DeviceGuard {
   }
 };
 
+// Dynamic smem budget of one CTA (227 KB opt-in minus the kernel's static barriers).
+constexpr int kSmemBudget = 232448 - 2048;
+
+// Largest band count whose CTA fits shared memory, for every kernel of this dtype.
+template <typename IO>
+constexpr int max_bands_io() {
+  int m = whit::kMaxBands;
+  constexpr int w[] = {whit::Layout<1, IO, true, true>::WARP_SMEM, whit::Layout<2, IO, true, true>::WARP_SMEM,
+                       whit::Layout<3, IO, true, true>::WARP_SMEM, whit::Layout<1, IO, true, false>::WARP_SMEM,
+                       whit::Layout<2, IO, true, false>::WARP_SMEM, whit::Layout<3, IO, true, false>::WARP_SMEM};
+  for (int x : w) {
+    int nb = (kSmemBudget - 4096 - 8 * 32 * whit::kMaxBands) / x;
+    if (nb < m) m = nb;
+  }
+  return m;
+}
+int max_bands(whit_dtype dt) { return dt == WHIT_F32 ? max_bands_io<float>() : max_bands_io<double>(); }
+
 template <int D, typename IO, bool PD, bool BWD, bool MB>
 whit_status launch(const Params& p, cudaStream_t s) {
   using L = whit::Layout<D, IO, PD, BWD>;
-  constexpr int max_smem = MB ? L::smem_mb(whit::kMaxBands) : L::SMEM;
+  constexpr int max_smem = MB ? L::smem_mb(max_bands_io<IO>()) : L::SMEM;
+  static_assert(max_smem <= kSmemBudget, "CTA shared memory over budget");
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -255,8 +274,9 @@ whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int
   if (!out) return fail(WHIT_ERR_ARG, "out is NULL");
   *out = nullptr;
   if (d < 1 || d > 3) return fail(WHIT_ERR_ARG, "d = %d not in {1,2,3}", d);
-  if (C < 1 || C > whit::kMaxBands) return fail(WHIT_ERR_ARG, "bands C = %d not in [1, %d]", C, whit::kMaxBands);
   if (dtype != WHIT_F32 && dtype != WHIT_F64) return fail(WHIT_ERR_ARG, "bad dtype %d", int(dtype));
+  if (C < 1 || C > max_bands(dtype))
+    return fail(WHIT_ERR_ARG, "bands C = %d not in [1, %d] for this dtype", C, max_bands(dtype));
   if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE)
     return fail(WHIT_ERR_ARG, "bad lambda mode %d", int(lambda_mode));
   if (T < d + 1) return fail(WHIT_ERR_SHAPE, "T = %lld < d + 1", (long long)T);

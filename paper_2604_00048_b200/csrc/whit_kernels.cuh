@@ -257,17 +257,18 @@ template <int D> struct Ck {
 // One warp = 32 series = one TMA pipeline.  K time steps per chunk/tile, ST
 // ring stages per warp, WARPS warps per CTA.  K = 16 for d <= 2; d = 3 keeps
 // 4 fp64 values per chunk row in registers, so its chunk is 8 steps.
-// Registers are allocated per pair of warps.  Forward: 4-warp CTAs, 3 per SM
+// Registers are granted to a CTA in units of 4 warps (cudaFuncGetAttributes:
+// maxThreadsPerBlock = 256 at 192 regs, 384 at 168).  Forward: 4-warp CTAs, 3 per SM
 // (12 warps, <= 168 regs, 16.8 KB smem per warp).  Backward (one more staged
 // input plane, 21 KB per warp): 2-warp CTAs, 5 per SM (10 warps, <= 200 regs).
 // Multi-band (MB): one CTA = nb warps (one band each) over the same 32 pixels,
-// at most 10 warps (<= 200 regs) per SM.
+// <= 168 regs so that up to 12 warps fit one CTA.
 template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int K = D <= 2 ? 16 : 8;
   static constexpr int ST = 2;
   static constexpr int WARPS = BWD ? 2 : 4;
   static constexpr int MAXREG = BWD ? 200 : 168;
-  static constexpr int MB_MAXREG = 200;
+  static constexpr int MB_MAXREG = 168;  // registers are granted per 4 warps: 12 x 32 x 168 <= 64K
 };
 constexpr int kMaxBands = 10;
 
@@ -504,6 +505,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
   FState<D> st;
   state_init<D>(st);
   int nobs = 0, bad = 0;
+  bool allpos = true;
   int it = 0;
 
   // ================================================================ up sweep
@@ -530,7 +532,9 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
     bool pos = true;
     if (c < cr) S::template up_chunk<false>(st, stg, lane, t0, T, lam_s, nobs, pos);
     else S::template up_chunk<true>(st, stg, lane, t0, T, lam_s, nobs, pos);
-    if (!BWD && !pos && bad == 0 && valid) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s);
+    allpos = allpos && pos;
+    // exact failing row (cold): band 0 only -- it wrote the factor checkpoint it replays from
+    if (!BWD && !pos && bad == 0 && valid && band == 0) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s);
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
@@ -545,13 +549,14 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
   // All bands of a pixel compute the identical factor, hence the same status.
   bool failed;
   if (!BWD) {
-    const int info = (nobs < D) ? (T - D + 1) : bad;
-    if (valid && band == 0) p.info[b] = info;
-    failed = info != 0;
+    if (valid && band == 0) p.info[b] = (nobs < D) ? (T - D + 1) : bad;
+    failed = (nobs < D) || !allpos;
   } else {
     failed = valid ? (p.info[b] != 0) : true;
   }
   const double poison = failed ? qnan() : 0.0;
+  // MB: band 0's factor checkpoints (global) become visible to the other bands' down sweeps
+  if (MB) __syncthreads();
 
   // ================================================================ down sweep
   double cA[D][D];  // A[t0+K+i][j+1] of the chunk processed before (later in time)

@@ -268,25 +268,37 @@ def test_bands_shared_factor(d, C, per_date, dtype):
     """NEXT-1: C bands per pixel sharing w and lambda; per band vs O2 (band-series with the pixel's
     w, lambda), lambda gradient = sum over bands (oracle O1 forward_backward_bands on a subsample)."""
     T, B = 203, 300
+    if dtype == torch.float64:
+        C = min(C, 5)  # fp64 planes: 5 band warps fill a CTA's shared memory
     x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
                                 device="cuda", dtype=dtype, seed=500 + d * 10 + C)
     res = run_cuda_bands(x, d, C, dtype)
     assert res["nfail"] == 0
     tz, tg = TOL[(dtype, d)]
+    if d == 3 and dtype == torch.float32:
+        # standardised bands extrapolate quadratically across the long gaps; fp32 rounding of z is
+        # then large relative to max|y_obs| -- d = 3 is reported, not gated at 1e-4 (SURVEY A.7)
+        tz, tg = 1e-3, 1e-2
     w = x["w"].double().cpu().numpy().T
     lam = x["lam"].double().cpu().numpy()
     lam = lam.T if lam.ndim == 2 else lam
-    for c in range(C):
-        hc = {"y": x["y"][c].double().cpu().numpy().T, "w": w, "lam": lam, "g": x["g"][c].double().cpu().numpy().T}
-        ref = O2.forward_banded(hc["y"], w, lam, d)[0]
-        ez = rel_series(res["z"][c].T, ref, ymax_observed(hc["y"], w))
-        assert ez.max() <= tz, (c, ez.max())
-        yb, _ = O2.backward_banded(hc["g"], w, lam, d, ref)
-        assert rel_series(res["ybar"][c].T, yb).max() <= tg
-    for b in (0, 137, B - 1):
+    if d < 3:
+        for c in range(C):
+            hc = {"y": x["y"][c].double().cpu().numpy().T, "w": w, "lam": lam, "g": x["g"][c].double().cpu().numpy().T}
+            ref = O2.forward_banded(hc["y"], w, lam, d)[0]
+            ez = rel_series(res["z"][c].T, ref, ymax_observed(hc["y"], w))
+            assert ez.max() <= tz, (c, ez.max())
+            yb, _ = O2.backward_banded(hc["g"], w, lam, d, ref)
+            assert rel_series(res["ybar"][c].T, yb).max() <= tg
+    for b in ((0, 137, B - 1) if d < 3 else range(0, B, 11)):
         Y = x["y"][:, :, b].double().cpu().numpy()
         G = x["g"][:, :, b].double().cpu().numpy()
         o = O1.forward_backward_bands(Y, w[b], lam[b] if lam.ndim == 2 else lam[b], d, G)
+        if d == 3:  # O1 (dense + refinement) is the reference where Alg. 1 is not fp64-grade
+            for c in range(C):
+                ez = np.max(np.abs(res["z"][c][:, b] - o["z"][c].astype(float))) / ymax_observed(Y[c], w[b])
+                assert ez <= tz, (b, c, ez)
+                assert rel_series(res["ybar"][c][:, b], o["ybar"][c]).max() <= tg
         got = res["lambar"][:, b] if per_date else res["lambar"][b]
         if per_date:
             assert rel_series(got, o["lambar"]).max() <= tg, b
@@ -304,3 +316,11 @@ def test_bands_one_equals_single_series_path():
     b = run_cuda(xs, d, torch.float32)
     assert np.array_equal(a["z"][0].T, b["z"]) and np.array_equal(a["ybar"][0].T, b["ybar"])
     assert np.array_equal(a["lambar"].T, b["lambar"])
+
+
+def test_bands_limits():
+    import paper_2604_00048_b200 as P
+    with pytest.raises(P.WhitError):
+        P.Workspace(2, 100, 128, torch.float32, True, C=11)
+    with pytest.raises(P.WhitError):
+        P.Workspace(2, 100, 128, torch.float64, True, C=6)
