@@ -35,6 +35,7 @@ from .whittaker import (  # noqa: F401
     backward,
     forward_backward,
     forward_backward_bands,
+    posterior_variance,
     is_spd,
 )
 from .banded import (  # noqa: F401

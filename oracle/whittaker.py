@@ -219,3 +219,23 @@ def forward_backward_bands(Y, w, lam, d: int, G, steps: int = 2) -> dict:
     if np.asarray(lam).ndim == 0:
         lamb = lamb.sum()
     return {"z": Z, "dz": apply_D(Z, d), "u": U, "ybar": ybar, "lambar": lamb, "lambar_terms": terms}
+
+
+def posterior_variance(w, lam, d: int, rows=None, steps: int = 2) -> np.ndarray:
+    """``diag(Omega^{-1})`` (NEXT-4): the pointwise posterior variance of z up to the noise
+    variance factor, behind the credibility band of Fig. 4 (its formula, eq. (2.2) of
+    the cited Bayesian Whittaker paper, is external -- reading R-15: under the Gaussian model
+    y ~ N(z, sigma^2 W^{-1}) with prior precision D^T Lambda D / sigma^2, Cov(z | y) =
+    sigma^2 Omega^{-1}).  Plain definition: ``Sigma_tt = e_t^T Omega^{-1} e_t`` by a refined
+    dense solve per requested row (all rows by default).  Long double.
+    """
+    Om = omega_dense(w, lam, d)
+    F = _Factor(Om)
+    T = Om.shape[0]
+    rows = range(T) if rows is None else rows
+    out = []
+    for t in rows:
+        e = np.zeros(T, dtype=LD)
+        e[t] = 1
+        out.append(F.solve(e, steps)[t])
+    return np.array(out, dtype=LD)

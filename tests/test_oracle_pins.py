@@ -489,3 +489,44 @@ def test_bands_shared_factor_fd_and_per_band(per_date):
     else:
         fd = (L(lam * np.exp(h)) - L(lam * np.exp(-h))) / (2 * h) / lam
     assert rel(o["lambar"], fd) < 1e-6
+
+
+# ----------------------------------------------------------------- posterior variance (NEXT-4)
+@pytest.mark.parametrize("d,T", [(1, 7), (2, 8), (3, 9)])
+def test_posterior_variance_exact_rational(d, T):
+    """diag(Omega^{-1}) == the exact rational inverse of half the Hessian of Eq. (1)."""
+    w = [Fraction(int(b)) for b in (rng.random(T) < 0.6)]
+    for i in range(d):
+        w[2 * i] = Fraction(1)
+    lam = dyadic(T - d, 1, 40)
+    _, H = exact_minimizer([Fraction(0)] * T, w, lam, d)
+    A = [[h / 2 for h in row] + [Fraction(int(i == j)) for j in range(T)] for i, row in enumerate(H)]
+    for c in range(T):
+        p = next(r for r in range(c, T) if A[r][c] != 0)
+        A[c], A[p] = A[p], A[c]
+        piv = A[c][c]
+        A[c] = [x / piv for x in A[c]]
+        for r in range(T):
+            if r != c and A[r][c] != 0:
+                f = A[r][c]
+                A[r] = [a - f * b for a, b in zip(A[r], A[c])]
+    exact = [float(A[i][T + i]) for i in range(T)]
+    got = O1.posterior_variance(np.array(w, float), np.array(lam, float), d)
+    assert rel(got, exact) < 1e-14
+
+
+def test_posterior_variance_properties():
+    """lambda = 0, w = 1 -> Omega = I -> variance 1; an extra observation never increases any
+    variance (Omega grows in the Loewner order); time reversal."""
+    T, d = 60, 2
+    assert np.allclose(O1.posterior_variance(np.ones(T), 0.0, d).astype(float), 1.0, rtol=0, atol=1e-15)
+    w = (rng.random(T) < 0.3).astype(float)
+    w[[0, 30, 59]] = 1
+    lam = 10 ** rng.uniform(0, 3, T - d)
+    v0 = O1.posterior_variance(w, lam, d).astype(float)
+    w2 = w.copy()
+    w2[np.flatnonzero(w == 0)[5]] = 1
+    v1 = O1.posterior_variance(w2, lam, d).astype(float)
+    assert np.all(v1 <= v0 * (1 + 1e-13))
+    vr = O1.posterior_variance(w[::-1].copy(), lam[::-1].copy(), d).astype(float)
+    assert rel(vr[::-1], v0) < 1e-13
