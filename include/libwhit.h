@@ -178,6 +178,20 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
 whit_status whit_backward_bands(const void* grad_z, whit_ws* factor_ws, const void* z, void* grad_y,
                                 void* grad_lambda);
 
+/* Posterior variance (NEXT-4): var[t][b] = (Omega^{-1})_{tt}, the pointwise
+ * variance of z up to the noise-variance factor sigma^2 (the credibility band
+ * of Fig. 4: under y ~ N(z, sigma^2 W^{-1}) with prior precision
+ * D^T Lambda D / sigma^2, Cov(z | y) = sigma^2 Omega^{-1}).  Computed by
+ * Takahashi's selected inversion on the same deviation-form banded factor
+ * (one up sweep, one down sweep; only the d x d window of Omega^{-1} next to
+ * the diagonal is ever formed).  w, lambda, d, T, B as in whit_forward; var
+ * [T][B] output.  Uses factor_ws's checkpoint area and info[] (info = T-d+1
+ * for fewer than d observed days, -1 for another non-positive pivot, var NaN);
+ * if (w, lambda) differ from the last forward's, that forward's backward is
+ * invalidated (WHIT_ERR_STATE).  Single-band workspaces only.  One launch. */
+whit_status whit_posterior_variance(const void* w, const void* lambda, int d, int64_t T, int64_t B, void* var,
+                                    whit_ws* factor_ws);
+
 /* SYNCHRONISES the workspace stream, then reports how many series of the
  * last forward failed (non-SPD, see "Numerical failure") in *n_failed and,
  * if host_info is non-NULL, copies info[0..B) (int32) to host_info. */

@@ -43,6 +43,7 @@ SIGNATURES = [
                                             ctypes.c_int, _VP, _SZ, _VP]),
     ("whit_forward_bands", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, _VP, _VP]),
     ("whit_backward_bands", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("whit_posterior_variance", ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_host_ws_bytes", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("whit_run_host", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                      _VP, _VP, _VP, _VP, _I64, ctypes.c_int, _VP, _SZ, _VP]),
@@ -147,6 +148,10 @@ def whit_backward_bands(grad_z, ws: Workspace, z, grad_y, grad_lambda):
 
 def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):
     _check(_lib.whit_backward(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)), "whit_backward")
+
+
+def whit_posterior_variance(w, lam, d: int, T: int, B: int, var, ws: Workspace):
+    _check(_lib.whit_posterior_variance(_ptr(w), _ptr(lam), d, T, B, _ptr(var), ws.handle), "whit_posterior_variance")
 
 
 def whit_failures(ws: Workspace, with_info: bool = False):

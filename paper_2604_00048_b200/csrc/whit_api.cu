@@ -211,6 +211,34 @@ whit_status dispatch(const whit_ws* ws, const Params& p) {
   return mb ? dispatch_pd<double, BWD, true>(ws, p) : dispatch_pd<double, BWD, false>(ws, p);
 }
 
+template <int D, typename IO, bool PD>
+whit_status launch_var(const Params& p, cudaStream_t s) {
+  using V = whit::VarLayout<D, IO, PD>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(whit::whit_var_kernel<D, IO, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    V::SMEM);
+  });
+  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  const long long per_cta = 32 * V::WARPS;
+  const long long grid = (p.B + per_cta - 1) / per_cta;
+  whit::whit_var_kernel<D, IO, PD><<<dim3((unsigned)grid), dim3((unsigned)per_cta), V::SMEM, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return WHIT_OK;
+}
+
+template <typename IO, bool PD>
+whit_status dispatch_var_d(int d, const Params& p, cudaStream_t s) {
+  switch (d) {
+    case 1: return launch_var<1, IO, PD>(p, s);
+    case 2: return launch_var<2, IO, PD>(p, s);
+    case 3: return launch_var<3, IO, PD>(p, s);
+  }
+  return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+}
+
 // Fill the tensor maps and plain pointers common to both directions.
 whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const void* w, const void* lam) {
   std::memset(p, 0, sizeof *p);
@@ -379,6 +407,31 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
 
 whit_status whit_backward_bands(const void* grad_z, whit_ws* ws, const void* z, void* grad_y, void* grad_lambda) {
   return whit_backward(grad_z, ws, z, grad_y, grad_lambda);
+}
+
+whit_status whit_posterior_variance(const void* w, const void* lambda, int d, int64_t T, int64_t B, void* var,
+                                    whit_ws* ws) {
+  if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (!w || !lambda || !var) return fail(WHIT_ERR_ARG, "NULL data pointer");
+  if (ws->nb != 1) return fail(WHIT_ERR_SHAPE, "posterior variance needs a single-band workspace");
+  if (d != ws->d || T != ws->T || B != ws->B)
+    return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
+                (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
+  if (!aligned16(w) || !aligned16(lambda) || !aligned16(var))
+    return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
+  if (var == w || var == lambda) return fail(WHIT_ERR_ARG, "var aliases an input");
+  DeviceGuard guard(ws->device);
+  if (!guard.ok) return fail(WHIT_ERR_CUDA, "cudaSetDevice(%d) failed", ws->device);
+  Params p;
+  whit_status st = fill_params(ws, &p, w /* unused rhs slot */, w, lambda);
+  if (st != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out0, var, ws->dt, B, T, chunk_k(d), 1)) != WHIT_OK) return st;
+  // the factor checkpoints are shared with the forward: a different (w, lambda) invalidates its backward
+  if (w != ws->w || lambda != ws->lam) ws->have_fwd = false;
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  if (ws->dt == WHIT_F32)
+    return pd ? dispatch_var_d<float, true>(d, p, ws->stream) : dispatch_var_d<float, false>(d, p, ws->stream);
+  return pd ? dispatch_var_d<double, true>(d, p, ws->stream) : dispatch_var_d<double, false>(d, p, ws->stream);
 }
 
 whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {

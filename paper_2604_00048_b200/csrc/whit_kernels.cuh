@@ -665,6 +665,219 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
   }
 }
 
+// ------------------------------------------------------------------ posterior variance (NEXT-4)
+// diag(Omega^{-1}) by Takahashi's selected inversion on the same deviation-form
+// factor (R-15).  With Sigma = Omega^{-1} = L^{-T} D^{-1} L^{-1}, rows descending:
+//   Sigma[t][t+l] = -sum_{k=1..d} L[t+k][t] Sigma[t+k][t+l]        (l = 1..d)
+//   Sigma[t][t]   = 1/D_t - sum_{k=1..d} L[t+k][t] Sigma[t][t+k]
+// needs only the d x d window of Sigma below-right of row t; L[t+k][t] = M_k + A[t+k][k].
+// Up sweep: factor + checkpoints (no right-hand side); down sweep: recompute the
+// chunk's factor, run the recurrence, stage Sigma[t][t] and TMA-store it.
+template <int D, typename IO, bool PD>
+struct VarLayout {
+  using L = Layout<D, IO, PD, false>;
+  static constexpr int K = L::K, ST = L::ST, ROW = L::ROW;
+  static constexpr int OFF_W = 0;
+  static constexpr int OFF_LAM = K * ROW;
+  static constexpr int STAGE = (OFF_LAM + (PD ? (K + D) * ROW : 0) + 127) / 128 * 128;
+  static constexpr int OUT = K * ROW;
+  static constexpr int WARP_SMEM = ST * STAGE + OUT;
+  static constexpr int WARPS = 4;
+  static constexpr int SMEM = WARPS * WARP_SMEM;
+  static constexpr uint32_t BYTES_UP = (K + (PD ? K : 0)) * ROW;
+  static constexpr uint32_t BYTES_DN = (K + (PD ? K + D : 0)) * ROW;
+};
+
+template <int D, typename IO, bool PD>
+__device__ __forceinline__ void issue_tile_var(const Params& p, unsigned char* stage, uint64_t* bar, int i, int C,
+                                               int c0) {
+  using V = VarLayout<D, IO, PD>;
+  const bool up = i < C;
+  const int c = up ? i : 2 * C - 1 - i;
+  const int t0 = c * V::K;
+  mbar_arrive_expect_tx(bar, up ? V::BYTES_UP : V::BYTES_DN);
+  tma_load_2d(stage + V::OFF_W, &p.tm_w, c0, t0, bar);
+  if (PD) {
+    if (up) tma_load_2d(stage + V::OFF_LAM, &p.tm_lam_up, c0, t0, bar);
+    else tma_load_2d(stage + V::OFF_LAM, &p.tm_lam_dn, c0, t0 - D, bar);
+  }
+}
+
+template <int D, typename IO, bool PD>
+__global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params p) {
+  using V = VarLayout<D, IO, PD>;
+  constexpr int K = V::K, ST = V::ST, WARPS = V::WARPS;
+  constexpr int NFAC = Ck<D>::NFAC;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[WARPS][ST];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = p.T, C = p.C, TmD = T - D;
+  const long long B = p.B;
+  const long long bw = ((long long)blockIdx.x * WARPS + warp) * 32;
+  if (bw >= B) return;
+  const long long b = bw + lane;
+  const bool valid = b < B;
+  unsigned char* ring = smem + warp * V::WARP_SMEM;
+  IO* so = reinterpret_cast<IO*>(ring + ST * V::STAGE);
+  uint64_t* bars = full_bar[warp];
+  const int ntiles = 2 * C;
+  if (lane == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < ST && i < ntiles; ++i) issue_tile_var<D, IO, PD>(p, ring + i * V::STAGE, &bars[i], i, C, (int)bw);
+  }
+  __syncwarp();
+  const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
+  const int cr = (T - D) / K;
+
+  FState<D> st;
+  state_init<D>(st);
+  int nobs = 0;
+  bool allpos = true;
+  int it = 0;
+  // ---------------------------------------------------------------- up sweep: factor only
+  for (int c = 0; c < C; ++c, ++it) {
+    const int s = it % ST;
+    mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
+    const unsigned char* stg = ring + s * V::STAGE;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + V::OFF_W) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + V::OFF_LAM) + lane;
+    const int t0 = c * K;
+    if (valid) {
+      double* ck = p.ck_fac + (long long)c * NFAC * B + b;
+      int f = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) ck[(long long)(f++) * B] = st.dl[i];
+#pragma unroll
+      for (int m = 0; m < D - 1; ++m)
+#pragma unroll
+        for (int k = 0; k < D - 1 - m; ++k) ck[(long long)(f++) * B] = st.ap[m][k];
+    }
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+      const int t = t0 + k;
+      if (t >= T) break;
+      const IO wio = t_w[k * 32];
+      const double w = to_f64<IO>(wio);
+      const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : (t < TmD ? lam_s : 0.0);
+      double A[D], Dt, idt, vt;
+      ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, A, Dt, idt, vt);
+      nobs += (wio > IO(0));
+      allpos = allpos && (Dt > 0.0);
+    }
+    __syncwarp();
+    if (lane == 0 && it + ST < ntiles) {
+      fence_proxy_async_smem();
+      issue_tile_var<D, IO, PD>(p, ring + s * V::STAGE, &bars[s], it + ST, C, (int)bw);
+    }
+  }
+  const bool failed = (nobs < D) || !allpos;
+  if (valid) p.info[b] = failed ? ((nobs < D) ? (T - D + 1) : -1) : 0;  // -1: pivot failure, row not located
+  const double poison = failed ? qnan() : 0.0;
+
+  // ---------------------------------------------------------------- down sweep: Takahashi
+  double cA[D][D];
+  double S[D][D];  // S[k][l] = Sigma[t+1+k][t+1+l], rows t+1..t+D
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) { cA[i][j] = 0.0; S[i][j] = poison; }
+  for (int c = C - 1; c >= 0; --c, ++it) {
+    const int s = it % ST;
+    mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
+    const unsigned char* stg = ring + s * V::STAGE;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + V::OFF_W) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + V::OFF_LAM) + lane;  // row k <-> t0 - D + k
+    const int t0 = c * K;
+    const bool ragged = (t0 + K > T);
+    if (valid) {
+      const double* ckf = p.ck_fac + (long long)c * NFAC * B + b;
+      int f = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) st.dl[i] = ckf[(long long)(f++) * B];
+#pragma unroll
+      for (int m = 0; m < D - 1; ++m)
+#pragma unroll
+        for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = ckf[(long long)(f++) * B];
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int tj = t0 - 1 - i;
+      st.v[i] = 0.0;
+      const double l = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : ((tj >= 0 && tj < TmD) ? lam_s : 0.0);
+      st.lm[i] = l;
+      st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO>::N>(l + st.dl[i]);
+    }
+    double idk[K];
+    double Ak[K][D];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int t = t0 + k;
+      const double w = to_f64<IO>(t_w[k * 32]);
+      double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
+      if (!PD) lt = (t < TmD) ? lt : 0.0;
+      double Dt, vt;
+      ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, Ak[k], Dt, idk[k], vt);
+      if (ragged && t >= T) {  // rows past the end: Sigma = 0 there, no coupling
+        idk[k] = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) Ak[k][j] = 0.0;
+      }
+    }
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
+#pragma unroll
+    for (int k = K - 1; k >= 0; --k) {
+      double Lc[D];  // L[t+j][t] - M_j = A[t+j][j]
+#pragma unroll
+      for (int j = 1; j <= D; ++j) Lc[j - 1] = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
+      double up[D];  // Sigma[t][t+l], l = 1..D
+#pragma unroll
+      for (int l = 1; l <= D; ++l) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = D; j >= 1; --j) {
+          const double sjl = (j <= l) ? S[j - 1][l - 1] : S[l - 1][j - 1];
+          acc = fma(-Mj(D, j), sjl, acc);
+          acc = fma(-Lc[j - 1], sjl, acc);
+        }
+        up[l - 1] = acc;
+      }
+      double dg = idk[k];
+#pragma unroll
+      for (int j = D; j >= 1; --j) {
+        dg = fma(-Mj(D, j), up[j - 1], dg);
+        dg = fma(-Lc[j - 1], up[j - 1], dg);
+      }
+      // shift the window: new row t becomes index 0
+#pragma unroll
+      for (int i = D - 1; i >= 1; --i)
+#pragma unroll
+        for (int j = D - 1; j >= i; --j) S[i][j] = S[i - 1][j - 1];
+      S[0][0] = dg;
+#pragma unroll
+      for (int l = 1; l < D; ++l) S[0][l] = up[l - 1];
+      so[k * 32 + lane] = from_f64<IO>(dg);
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) cA[i][j] = Ak[i][j];
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(&p.tm_out0, so, (int)bw, t0, 0);
+      bulk_commit();
+      if (it + ST < ntiles) {
+        fence_proxy_async_smem();
+        issue_tile_var<D, IO, PD>(p, ring + s * V::STAGE, &bars[s], it + ST, C, (int)bw);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait0();
+}
+
 // Count of failed series (info != 0) for whit_failures.
 __global__ void count_failures(const int32_t* __restrict__ info, long long B, unsigned long long* out) {
   unsigned long long n = 0;

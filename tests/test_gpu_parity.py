@@ -324,3 +324,49 @@ def test_bands_limits():
         P.Workspace(2, 100, 128, torch.float32, True, C=11)
     with pytest.raises(P.WhitError):
         P.Workspace(2, 100, 128, torch.float64, True, C=6)
+
+
+def run_cuda_var(x: dict, d: int, dtype):
+    import paper_2604_00048_b200 as P
+
+    w, lam = x["w"].to(dtype).contiguous(), x["lam"].to(dtype).contiguous()
+    T, B = w.shape
+    ws = P.Workspace(d, T, B, dtype, lam.dim() == 2)
+    var = torch.empty_like(w)
+    P.whit_posterior_variance(w, lam, d, T, B, var, ws)
+    torch.cuda.synchronize()
+    return var.double().cpu().numpy().T
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_posterior_variance_vs_oracle(d, per_date, dtype):
+    """NEXT-4: diag(Omega^{-1}) by Takahashi on the deviation-form factor vs the refined dense
+    definition (O1), ragged T and B; per series max|var - ref| / max|ref|."""
+    T, B = 203, 132
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", dtype=dtype, seed=700 + d)
+    var = run_cuda_var(x, d, dtype)
+    h = host_inputs(x)
+    tol = {torch.float32: 1e-4, torch.float64: 1e-10 if d < 3 else 1e-8}[dtype]
+    for b in range(0, B, 7):
+        ref = O1.posterior_variance(h["w"][b], h["lam"][b], d)
+        e = rel_series(var[b], ref).max()
+        assert e <= tol, (b, e)
+
+
+def test_posterior_variance_full_size_sampled():
+    """hetero shape (B = 262,144, T = 3,288, fp32): sampled series and rows vs O1."""
+    d = 2
+    x = synth.make_inputs("hetero", device="cuda")
+    var = run_cuda_var({"w": x["w"], "lam": x["lam"]}, d, torch.float32)
+    B = x["w"].shape[1]
+    assert np.all(np.isfinite(var)) and np.all(var > 0)
+    rows = np.array([0, 1, 500, 1600, 3000, 3196, 3250, 3286, 3287])
+    for b in _sample(B, 4):
+        w = x["w"][:, b].double().cpu().numpy()
+        lam = x["lam"][:, b].double().cpu().numpy()
+        ref = O1.posterior_variance(w, lam, d, rows=rows).astype(float)
+        allref = np.max(np.abs(ref))
+        assert np.max(np.abs(var[b][rows] - ref)) / allref <= 1e-4
