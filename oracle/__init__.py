@@ -36,6 +36,7 @@ from .whittaker import (  # noqa: F401
     forward_backward,
     forward_backward_bands,
     posterior_variance,
+    mse_loss_grad,
     is_spd,
 )
 from .banded import (  # noqa: F401

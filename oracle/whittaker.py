@@ -239,3 +239,16 @@ def posterior_variance(w, lam, d: int, rows=None, steps: int = 2) -> np.ndarray:
         e[t] = 1
         out.append(F.solve(e, steps)[t])
     return np.array(out, dtype=LD)
+
+
+def mse_loss_grad(z, y, loss_w):
+    """NEXT-3: the training loss of the paper in the form of its MSE metric,
+    ``L = T^{-1} sum_t lw_t (z_t - y_t)^2``, and its cotangent ``g = dL/dz = 2 T^{-1} lw (z - y)``.
+    ``lw`` selects the scored dates (e.g. the randomly held-out ones, whose W_tt was set to 0 in
+    the smoother); terms with ``lw_t = 0`` are exactly 0 (their y may be NaN).  Long double."""
+    z = np.asarray(z).astype(LD)
+    y = np.asarray(y, dtype=np.float64)
+    lw = np.asarray(loss_w, dtype=np.float64)
+    T = z.shape[-1]
+    e = np.where(lw != 0, z - y.astype(LD), LD(0))
+    return (lw.astype(LD) * e * e).sum(axis=-1) / T, 2 * lw.astype(LD) * e / T

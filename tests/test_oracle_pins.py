@@ -530,3 +530,32 @@ def test_posterior_variance_properties():
     assert np.all(v1 <= v0 * (1 + 1e-13))
     vr = O1.posterior_variance(w[::-1].copy(), lam[::-1].copy(), d).astype(float)
     assert rel(vr[::-1], v0) < 1e-13
+
+
+# ----------------------------------------------------------------- fused masked-MSE (NEXT-3)
+def test_mse_chain_rule_fd():
+    """The training step: L(y, lam) = T^-1 sum lw (z(y, lam) - y_ref)^2 with z from Eq. (3);
+    backward(g = dL/dz) + the explicit dL/dy_ref term equals central finite differences."""
+    T, d = 40, 2
+    y = rng.normal(size=T)
+    w = (rng.random(T) < 0.6).astype(float)
+    w[:3] = 1
+    lw = ((rng.random(T) < 0.3) & (w == 0)).astype(float)  # score held-out dates
+    lw[5] = 1.0
+    w[5] = 0.0
+    lam = 10 ** rng.uniform(0, 2, T - d)
+    z, _ = O1.forward(y, w, lam, d)
+    loss, g = O1.mse_loss_grad(z, y, lw)
+    ybar, lambar = O1.backward(g.astype(float), w, lam, d, z)
+
+    def Lf(yv, lv):
+        zz, _ = O1.forward(yv, w, lv, d)
+        return float(O1.mse_loss_grad(zz, yv, lw)[0])
+
+    h = 1e-6
+    fd_l = np.array([(Lf(y, lam * np.exp(h * e)) - Lf(y, lam * np.exp(-h * e))) / (2 * h) for e in np.eye(T - d)]) / lam
+    assert rel(lambar, fd_l) < 1e-6
+    # y enters twice: through z (ybar) and as the reference (-g)
+    fd_y = np.array([(Lf(y + h * e, lam) - Lf(y - h * e, lam)) / (2 * h) for e in np.eye(T)])
+    assert rel(ybar.astype(float) - g.astype(float), fd_y) < 1e-6
+    assert abs(float(loss) - np.sum(lw * (z.astype(float) - y) ** 2) / T) < 1e-15
