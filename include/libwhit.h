@@ -178,6 +178,20 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
 whit_status whit_backward_bands(const void* grad_z, whit_ws* factor_ws, const void* z, void* grad_y,
                                 void* grad_lambda);
 
+/* Forward fused with the training loss (NEXT-3): the paper trains with a
+ * masking strategy and an MSE loss, the MSE of P:222:
+ *     loss[b]   = T^{-1} sum_t loss_w[t][b] (z[t][b] - y[t][b])^2
+ *     grad_z    = dL/dz with L = sum_b loss[b]:  2 T^{-1} loss_w (z - y)
+ * y is both the smoother input (through W y: held-out dates have w = 0) and
+ * the reference (the caller may pre-fill y at cloud/edge gaps with the
+ * nearest valid value, P:197 -- w = 0 there, so the solve never reads it).
+ * loss_w [T][B] selects / weights the scored dates (0 = not scored; y may be
+ * NaN there).  Same z and factor_ws state as whit_forward: feed grad_z to
+ * whit_backward.  Saves the separate loss/gradient pass over z (and the
+ * round trip of g).  Single-band workspaces.  One launch. */
+whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, const void* loss_w, int d, int64_t T,
+                             int64_t B, void* z, void* grad_z, void* loss, whit_ws* factor_ws);
+
 /* Posterior variance (NEXT-4): var[t][b] = (Omega^{-1})_{tt}, the pointwise
  * variance of z up to the noise-variance factor sigma^2 (the credibility band
  * of Fig. 4: under y ~ N(z, sigma^2 W^{-1}) with prior precision

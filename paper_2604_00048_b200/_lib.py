@@ -43,6 +43,7 @@ SIGNATURES = [
                                             ctypes.c_int, _VP, _SZ, _VP]),
     ("whit_forward_bands", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, _VP, _VP]),
     ("whit_backward_bands", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("whit_forward_mse", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP, _VP, _VP]),
     ("whit_posterior_variance", ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_host_ws_bytes", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("whit_run_host", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
@@ -148,6 +149,11 @@ def whit_backward_bands(grad_z, ws: Workspace, z, grad_y, grad_lambda):
 
 def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):
     _check(_lib.whit_backward(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)), "whit_backward")
+
+
+def whit_forward_mse(y, w, lam, loss_w, d: int, T: int, B: int, z, grad_z, loss, ws: Workspace):
+    _check(_lib.whit_forward_mse(_ptr(y), _ptr(w), _ptr(lam), _ptr(loss_w), d, T, B, _ptr(z), _ptr(grad_z), _ptr(loss),
+                                 ws.handle), "whit_forward_mse")
 
 
 def whit_posterior_variance(w, lam, d: int, T: int, B: int, var, ws: Workspace):

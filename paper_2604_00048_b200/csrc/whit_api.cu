@@ -164,15 +164,15 @@ constexpr int max_bands_io() {
 }
 int max_bands(whit_dtype dt) { return dt == WHIT_F32 ? max_bands_io<float>() : max_bands_io<double>(); }
 
-template <int D, typename IO, bool PD, bool BWD, bool MB>
+template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false>
 whit_status launch(const Params& p, cudaStream_t s) {
-  using L = whit::Layout<D, IO, PD, BWD>;
+  using L = whit::Layout<D, IO, PD, BWD, LOSS>;
   constexpr int max_smem = MB ? L::smem_mb(max_bands_io<IO>()) : L::SMEM;
   static_assert(max_smem <= kSmemBudget, "CTA shared memory over budget");
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB>,
+    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
   });
   if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
@@ -181,7 +181,7 @@ whit_status launch(const Params& p, cudaStream_t s) {
   const long long per_cta = MB ? 32 : threads;
   const long long grid = (p.B + per_cta - 1) / per_cta;
   const int smem = MB ? L::smem_mb(p.nb) : L::SMEM;
-  whit::whit_kernel<D, IO, PD, BWD, MB><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
+  whit::whit_kernel<D, IO, PD, BWD, MB, LOSS><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
@@ -209,6 +209,16 @@ whit_status dispatch(const whit_ws* ws, const Params& p) {
   if (ws->dt == WHIT_F32)
     return mb ? dispatch_pd<float, BWD, true>(ws, p) : dispatch_pd<float, BWD, false>(ws, p);
   return mb ? dispatch_pd<double, BWD, true>(ws, p) : dispatch_pd<double, BWD, false>(ws, p);
+}
+
+template <typename IO, bool PD>
+whit_status dispatch_loss_d(int d, const Params& p, cudaStream_t s) {
+  switch (d) {
+    case 1: return launch<1, IO, PD, false, false, true>(p, s);
+    case 2: return launch<2, IO, PD, false, false, true>(p, s);
+    case 3: return launch<3, IO, PD, false, false, true>(p, s);
+  }
+  return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
 }
 
 template <int D, typename IO, bool PD>
@@ -367,6 +377,43 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
   ws->have_fwd = false;
   st = dispatch<false>(ws, p);
+  if (st != WHIT_OK) return st;
+  ws->have_fwd = true;
+  ws->w = w; ws->lam = lambda; ws->z = z;
+  return WHIT_OK;
+}
+
+whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, const void* loss_w, int d, int64_t T,
+                             int64_t B, void* z, void* grad_z, void* loss, whit_ws* ws) {
+  if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (!y || !w || !lambda || !loss_w || !z || !grad_z || !loss) return fail(WHIT_ERR_ARG, "NULL data pointer");
+  if (ws->nb != 1) return fail(WHIT_ERR_SHAPE, "the fused loss needs a single-band workspace");
+  if (d != ws->d || T != ws->T || B != ws->B)
+    return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
+                (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
+  if (!aligned16(y) || !aligned16(w) || !aligned16(lambda) || !aligned16(loss_w) || !aligned16(z) ||
+      !aligned16(grad_z) || !aligned16(loss))
+    return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
+  for (const void* o : {(const void*)z, (const void*)grad_z, (const void*)loss})
+    if (o == y || o == w || o == lambda || o == loss_w) return fail(WHIT_ERR_ARG, "an output aliases an input");
+  if (z == grad_z || z == loss || grad_z == loss) return fail(WHIT_ERR_ARG, "outputs alias each other");
+  DeviceGuard guard(ws->device);
+  if (!guard.ok) return fail(WHIT_ERR_CUDA, "cudaSetDevice(%d) failed", ws->device);
+  Params p;
+  whit_status st = fill_params(ws, &p, y, w, lambda);
+  if (st != WHIT_OK) return st;
+  const int kK = chunk_k(d);
+  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_lw, loss_w, ws->dt, B, T, kK)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out2, grad_z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
+  p.loss = loss;
+  ws->have_fwd = false;
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  if (ws->dt == WHIT_F32)
+    st = pd ? dispatch_loss_d<float, true>(d, p, ws->stream) : dispatch_loss_d<float, false>(d, p, ws->stream);
+  else
+    st = pd ? dispatch_loss_d<double, true>(d, p, ws->stream) : dispatch_loss_d<double, false>(d, p, ws->stream);
   if (st != WHIT_OK) return st;
   ws->have_fwd = true;
   ws->w = w; ws->lam = lambda; ws->z = z;

@@ -58,6 +58,9 @@ struct Params {
   const void* lam_scalar; // [B] (scalar lambda mode)
   const void* lam_plane;  // [T-d][B] (per-date mode; read directly only by the cold failure path)
   void* out1;             // backward, scalar lambda: grad_lambda [B]
+  CUtensorMap tm_lw;      // LOSS: loss weights [T][B], box {32, K}
+  CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
+  void* loss;             // LOSS: per-series loss [B]
   double* ck_fac;         // factor checkpoints [C][NFAC][B] (written by band 0, read by all bands)
   double* ck_rhs_f;       // forward rhs checkpoints [C][nb][d][B]
   double* ck_rhs_b;       // backward rhs checkpoints [C][nb][d][B]
@@ -272,28 +275,29 @@ template <typename IO, int D, bool BWD> struct Tile {
 };
 constexpr int kMaxBands = 10;
 
-template <int D, typename IO, bool PD, bool BWD> struct Layout {
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false> struct Layout {
   static constexpr int K = Tile<IO, D, BWD>::K, ST = Tile<IO, D, BWD>::ST, WARPS = Tile<IO, D, BWD>::WARPS;
   static constexpr int ROW = 32 * (int)sizeof(IO);  // bytes of one staged time row (one warp)
   static constexpr int OFF_RHS = 0;
   static constexpr int OFF_W = K * ROW;
   static constexpr int OFF_LAM = 2 * K * ROW;
   static constexpr int OFF_DZ = OFF_LAM + (PD ? (K + D) * ROW : 0);
-  static constexpr int STAGE = (OFF_DZ + (BWD ? K * ROW : 0) + 127) / 128 * 128;
+  static constexpr int OFF_LW = OFF_DZ + (BWD ? K * ROW : 0);  // LOSS (forward): loss-weight tile
+  static constexpr int STAGE = (OFF_LW + (LOSS ? K * ROW : 0) + 127) / 128 * 128;
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
-  static constexpr int WARP_SMEM = ST * STAGE + 2 * OUT;     // ring + out0 + out1
+  static constexpr int WARP_SMEM = ST * STAGE + (LOSS ? 3 : 2) * OUT;  // ring + out0 + out1 (+ out2)
   static constexpr int SMEM = WARPS * WARP_SMEM;
   // multi-band CTA of nb warps: rings + reduction tile + scalar slots
   static constexpr int smem_mb(int nb) { return nb * WARP_SMEM + OUT + nb * 32 * 8; }
   static constexpr uint32_t BYTES_UP = (2 * K + (PD ? K : 0)) * ROW;
-  static constexpr uint32_t BYTES_DN = (2 * K + (PD ? K + D : 0) + (BWD ? K : 0)) * ROW;
+  static constexpr uint32_t BYTES_DN = (2 * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
 };
 
 // Issue tile i (up sweep tiles 0..C-1, then down sweep C-1..0) of one warp.
-template <int D, typename IO, bool PD, bool BWD>
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false>
 __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage, uint64_t* bar, int i, int C,
                                            int c0, int band) {
-  using L = Layout<D, IO, PD, BWD>;
+  using L = Layout<D, IO, PD, BWD, LOSS>;
   const bool up = i < C;
   const int c = up ? i : 2 * C - 1 - i;
   const int t0 = c * L::K;
@@ -305,12 +309,13 @@ __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage
     else tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_dn, c0, t0 - D, bar);
   }
   if (BWD && !up) tma_load_3d(stage + L::OFF_DZ, &p.tm_dz, c0, t0, band, bar);
+  if (LOSS && !up) tma_load_2d(stage + L::OFF_LW, &p.tm_lw, c0, t0, bar);
 }
 
 // ------------------------------------------------------------------ per-thread sweep bodies
-template <int D, typename IO, bool PD, bool BWD>
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false>
 struct Sweep {
-  using L = Layout<D, IO, PD, BWD>;
+  using L = Layout<D, IO, PD, BWD, LOSS>;
   static constexpr int K = L::K;
 
   // ---- up sweep over one chunk (rows t0..t0+K-1); RAGGED: the chunk reaches row T-D or beyond
@@ -386,7 +391,8 @@ struct Sweep {
   template <bool RAGGED>
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
-                                                    int T, double lam_s, IO* so0, IO* so1) {
+                                                    int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
+                                                    double two_over_T = 0.0) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -431,6 +437,14 @@ struct Sweep {
       if (!BWD) {
         so0[k * 32] = from_f64<IO>(z);
         so1[k * 32] = from_f64<IO>(dz);
+        if (LOSS) {  // masked MSE: L += lw (z - y)^2 / T, g = 2 lw (z - y) / T
+          const IO lw = reinterpret_cast<const IO*>(stg + L::OFF_LW)[lane + k * 32];
+          const IO yr = reinterpret_cast<const IO*>(stg + L::OFF_RHS)[lane + k * 32];
+          const double e = (lw != IO(0)) ? z - to_f64<IO>(yr) : 0.0;  // unscored dates: exactly 0 (y may be NaN)
+          const double lwe = to_f64<IO>(lw) * e;
+          so2[k * 32] = from_f64<IO>(two_over_T * lwe);
+          if (!RAGGED || t < T) lam_acc = fma(lwe, e, lam_acc);  // (forward: lam_acc holds the loss sum)
+        }
       } else {
         if (sizeof(IO) == 4 && PD) {
           // fp32 I/O: w*u and -(Du)(Dz) formed from u, Du rounded once to fp32 (<= 1.5 ulp fp32)
@@ -461,11 +475,12 @@ struct Sweep {
 //               the factor (band 0 writes its checkpoints, every band reads
 //               them) and, in the backward, reduce -(Du_c)(Dz_c) over bands in
 //               shared memory in band order (deterministic).
-template <int D, typename IO, bool PD, bool BWD, bool MB>
-__global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>::MAXREG))
+template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false>
+__global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Tile<IO, D, BWD>::MAXREG))
     whit_kernel(const __grid_constant__ Params p) {
-  using L = Layout<D, IO, PD, BWD>;
-  using S = Sweep<D, IO, PD, BWD>;
+  static_assert(!LOSS || (!BWD && !MB), "the fused loss is a single-band forward variant");
+  using L = Layout<D, IO, PD, BWD, LOSS>;
+  using S = Sweep<D, IO, PD, BWD, LOSS>;
   constexpr int K = L::K, ST = L::ST;
   constexpr int NFAC = Ck<D>::NFAC;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -482,6 +497,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
   unsigned char* ring = smem + warp * L::WARP_SMEM;
   IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);
   IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
+  IO* so2 = reinterpret_cast<IO*>(ring + ST * L::STAGE + 2 * L::OUT);  // LOSS only
   uint64_t* bars = full_bar[warp];
   const int ntiles = 2 * C;
   // MB backward: per-CTA reduction tile (K rows x 32 pixels) and scalar slots
@@ -493,7 +509,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
     for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < ST && i < ntiles; ++i)
-      issue_tile<D, IO, PD, BWD>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw, band);
   }
   __syncwarp();
 
@@ -538,7 +554,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }
   }
 
@@ -612,15 +628,19 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
     // the staging tiles must have been read by the previous chunk's TMA stores
     if (lane == 0) bulk_wait_read0();
     __syncwarp();
+    const double two_over_T = 2.0 / (double)T;
     if (c < cr)
-      S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane);
+      S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
+                                    so2 + lane, two_over_T);
     else
-      S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane);
+      S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
+                                   so2 + lane, two_over_T);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
     if (lane == 0) {
       tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
       if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
+      if (LOSS) tma_store_3d(&p.tm_out2, so2, (int)bw, t0, 0);
       if (BWD && PD && !MB) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
       bulk_commit();
     }
@@ -645,11 +665,12 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : Tile<IO, D, BWD>
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }
   }
 #undef WHIT_LOAD_CK
   if (lane == 0) bulk_wait0();  // stores complete before the CTA exits (smem stays valid)
+  if (LOSS && valid) reinterpret_cast<IO*>(p.loss)[b] = from_f64<IO>(lam_acc / (double)T);
   if (BWD && !PD) {
     if (MB) {  // scalar lambda: reduce the per-band sums in band order
       redS[warp * 32 + lane] = lam_acc;

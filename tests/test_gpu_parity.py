@@ -370,3 +370,40 @@ def test_posterior_variance_full_size_sampled():
         ref = O1.posterior_variance(w, lam, d, rows=rows).astype(float)
         allref = np.max(np.abs(ref))
         assert np.max(np.abs(var[b][rows] - ref)) / allref <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+def test_fused_mse_forward(dtype, per_date):
+    """NEXT-3: whit_forward_mse == whit_forward (z bitwise) + the oracle's masked-MSE loss and
+    cotangent; the cotangent drives whit_backward to the oracle gradients of the training step.
+    Held-out dates: w = 0, scored (lw = 1), y kept; other unobserved dates carry NaN y."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 203, 132
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", dtype=dtype, seed=900)
+    y, w, lam = x["y"], x["w"].clone(), x["lam"]
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    held = (torch.rand(w.shape, device="cuda", generator=gen) < 0.2) & (w > 0)
+    w[held] = 0
+    lw = held.to(dtype)
+    y = torch.where((w > 0) | held, y, torch.full_like(y, float("nan")))
+    ws = P.Workspace(d, T, B, dtype, per_date)
+    z, gz, loss = torch.empty_like(y), torch.empty_like(y), torch.empty(B, dtype=dtype, device="cuda")
+    P.whit_forward_mse(y, w, lam, lw, d, T, B, z, gz, loss, ws)
+    gy, gl = torch.empty_like(y), torch.empty_like(lam)
+    P.whit_backward(gz, ws, z, gy, gl)
+    ref = run_cuda({"y": y, "w": w, "lam": lam, "g": gz}, d, dtype, backward=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.double().cpu().numpy().T, ref["z"])
+    h = host_inputs({"y": y, "w": w, "lam": lam})
+    lwh = lw.double().cpu().numpy().T
+    tz, tg = TOL[(dtype, d)]
+    for b in range(0, B, 9):
+        z1, _ = O1.forward(h["y"][b], h["w"][b], h["lam"][b], d)
+        l1, g1 = O1.mse_loss_grad(z1, np.nan_to_num(h["y"][b]), lwh[b])
+        assert abs(loss[b].item() - float(l1)) <= tg * max(float(l1), 1e-300), b
+        assert rel_series(gz[:, b].double().cpu().numpy(), g1).max() <= tg
+        o = O1.backward(g1.astype(float), h["w"][b], h["lam"][b], d, z1)
+        assert rel_series(gy[:, b].double().cpu().numpy(), o[0]).max() <= tg
