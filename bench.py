@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--impl", default="libwhit", choices=["libwhit", "reference"])
     ap.add_argument("--config", default="hetero", choices=["hetero", "homo", "toy", "s2tile"])
     ap.add_argument("--io", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--op", default="fwdbwd", choices=["fwdbwd", "train", "variance"],
+                    help="fwdbwd: whit_forward + whit_backward (the BASELINE metric); train: whit_forward_mse "
+                         "(fused masked-MSE, NEXT-3) + whit_backward; variance: whit_posterior_variance (NEXT-4)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -297,6 +300,9 @@ def run_libwhit(args):
     gy = torch.empty_like(y)
     gl = torch.empty_like(lam)
 
+    if args.op != "fwdbwd":
+        return run_op(args, P, x, wsp, d, T, B, io, dev, stream, ws_n, rank)
+
     def step():
         P.whit_forward(y, w, lam, d, T, B, z, wsp)
         P.whit_backward(g, wsp, z, gy, gl)
@@ -386,6 +392,54 @@ def run_libwhit(args):
         print(json.dumps(line), flush=True)
     if ws_n > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_op(args, P, x, wsp, d, T, B, io, dev, stream, ws_n, rank):
+    """NEXT-row measurements on the same workload: 'train' = whit_forward_mse (the paper's masked
+    MSE on 20 % held-out dates) + whit_backward; 'variance' = whit_posterior_variance."""
+    import torch
+    y, w, lam = x["y"], x["w"], x["lam"]
+    if args.op == "train":
+        gen = torch.Generator(device=dev).manual_seed(1)
+        held = (torch.rand(w.shape, device=dev, generator=gen) < 0.2) & (w > 0)
+        w = w.masked_fill(held, 0.0)
+        lw = held.to(io)
+        del held
+        z, gz, gy = torch.empty_like(y), torch.empty_like(y), torch.empty_like(y)
+        gl, loss = torch.empty_like(lam), torch.empty(B, dtype=io, device=dev)
+
+        def step():
+            P.whit_forward_mse(y, w, lam, lw, d, T, B, z, gz, loss, wsp)
+            P.whit_backward(gz, wsp, z, gy, gl)
+        metric, launches = "training steps (fused masked-MSE fwd + bwd) series/s", 2
+    else:
+        var = torch.empty_like(w)
+
+        def step():
+            P.whit_posterior_variance(w, lam, d, T, B, var, wsp)
+        metric, launches = "posterior variance diag(Omega^-1) series/s", 1
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk = ClockSampler(dev.index or 0)
+    clk.start()
+    time.sleep(0.15)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
+    if rank == 0:
+        print(json.dumps({"metric": metric, "value": ws_n * B / (ms / 1e3), "unit": UNIT, "n_gpus": ws_n,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": args.config, "op": args.op, "B_per_gpu": B, "T": T, "d": d,
+                                     "io": args.io, "l2": "inputs larger than L2"},
+                          "gpu_launches": launches * args.steps, "clocks": clocks}), flush=True)
     return 0
 
 
