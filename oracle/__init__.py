@@ -37,6 +37,9 @@ from .whittaker import (  # noqa: F401
     forward_backward_bands,
     posterior_variance,
     mse_loss_grad,
+    difference_matrix_times,
+    omega_dense_times,
+    forward_backward_times,
     is_spd,
 )
 from .banded import (  # noqa: F401

@@ -252,3 +252,52 @@ def mse_loss_grad(z, y, loss_w):
     T = z.shape[-1]
     e = np.where(lw != 0, z - y.astype(LD), LD(0))
     return (lw.astype(LD) * e * e).sum(axis=-1) / T, 2 * lw.astype(LD) * e / T
+
+
+# ----------------------------------------------------------------------------- irregular grid (NEXT-2)
+def difference_matrix_times(times, d: int, dtype=LD) -> np.ndarray:
+    """Order-d difference operator on uneven acquisition times (the dspline divided
+    differences it cites, as restated by SPEC S:130): D^(1) = plain forward differences,
+    D^(m+1) = Bdiff . diag(m / (t_{i+m} - t_i)) . D^(m).  Row r spans dates r..r+d.
+    On unit-spaced times this is exactly the binomial stencil (R-3)."""
+    t = np.asarray(times, dtype=np.float64).astype(dtype)
+    T = t.shape[0]
+    if T < d + 1:
+        raise ValueError("need T >= d + 1")
+    Dm = np.zeros((T - 1, T), dtype=dtype)
+    Dm[np.arange(T - 1), np.arange(T - 1)] = -1
+    Dm[np.arange(T - 1), np.arange(1, T)] = 1
+    for m in range(1, d):
+        n = Dm.shape[0]
+        scale = dtype(m) / (t[m:m + n] - t[:n])
+        S = Dm * scale[:, None]
+        Dm = S[1:] - S[:-1]
+    return Dm
+
+
+def omega_dense_times(w, lam, times, d: int, dtype=LD) -> np.ndarray:
+    """Omega = W + D^T diag(lam) D with D from the acquisition times, as sum_r lam_r d_r d_r^T."""
+    w = np.asarray(w, dtype=np.float64)
+    T = w.shape[0]
+    lt = lam_tilde(lam, T, d)
+    Dm = difference_matrix_times(times, d, dtype)
+    Om = np.zeros((T, T), dtype=dtype)
+    Om[np.arange(T), np.arange(T)] = w.astype(dtype)
+    for r in range(T - d):
+        c = Dm[r, r:r + d + 1]
+        Om[r:r + d + 1, r:r + d + 1] += dtype(lt[r]) * np.outer(c, c)
+    return Om
+
+
+def forward_backward_times(y, w, lam, times, d: int, g, steps: int = 2) -> dict:
+    """Eq. (3)-(5) on an irregular grid (z, dz = D z, u, ybar, lambar), long double."""
+    Om = omega_dense_times(w, lam, times, d)
+    F = _Factor(Om)
+    z = F.solve(_rhs(y, w), steps)
+    u = F.solve(np.asarray(g, dtype=np.float64).astype(LD), steps)
+    Dm = difference_matrix_times(times, d)
+    dz, du = Dm @ z, Dm @ u
+    lamb = -du * dz
+    if np.asarray(lam).ndim == 0:
+        lamb = lamb.sum()
+    return {"z": z, "dz": dz, "u": u, "ybar": np.asarray(w, dtype=np.float64).astype(LD) * u, "lambar": lamb}

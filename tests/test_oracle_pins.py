@@ -559,3 +559,100 @@ def test_mse_chain_rule_fd():
     fd_y = np.array([(Lf(y + h * e, lam) - Lf(y - h * e, lam)) / (2 * h) for e in np.eye(T)])
     assert rel(ybar.astype(float) - g.astype(float), fd_y) < 1e-6
     assert abs(float(loss) - np.sum(lw * (z.astype(float) - y) ** 2) / T) < 1e-15
+
+
+# ----------------------------------------------------------------- irregular grid (NEXT-2)
+def _uneven_times(T, lo=1, hi=12):
+    return np.cumsum(rng.integers(lo, hi, size=T)).astype(float)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_times_operator_golden_and_unit_grid(d):
+    """SPEC S:134 worked row; unit-spaced times reduce exactly to the daily stencil (R-3)."""
+    g = GOLD["divided_difference_uneven"]
+    assert O1.difference_matrix_times(g["times"], g["order"]).astype(float)[0].tolist() == g["row"]
+    T = 20
+    assert np.array_equal(O1.difference_matrix_times(np.arange(T) + 7.0, d).astype(float), O1.difference_matrix(T, d))
+    lam = 10 ** rng.uniform(0, 3, T - d)
+    w = (rng.random(T) < 0.6).astype(float)
+    w[:d] = 1
+    y, gg = rng.normal(size=T), rng.normal(size=T)
+    a = O1.forward_backward_times(y, w, lam, np.arange(T, dtype=float), d, gg)
+    b = O1.forward_backward(y, w, lam, d, gg)
+    for k in ("z", "ybar", "lambar"):
+        assert rel(a[k], b[k]) < 1e-15
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_times_polynomial_annihilation_and_passthrough(d):
+    """On ANY increasing grid the rows annihilate t^0..t^(d-1) (divided differences), so a polynomial
+    of degree < d in t passes through the smoother unchanged, gaps included."""
+    T = 60
+    t = _uneven_times(T)
+    Dm = O1.difference_matrix_times(t, d).astype(float)
+    for p in range(d):
+        assert np.max(np.abs(Dm @ (t / t[-1]) ** p)) < 1e-12
+    assert np.max(np.abs(Dm @ (t / t[-1]) ** d)) > 1e-9
+    coef = rng.normal(size=d)
+    y = sum(c * (t / t[-1]) ** k for k, c in enumerate(coef))
+    w = (rng.random(T) < 0.3).astype(float)
+    w[[1, 20, 40]] = 1
+    o = O1.forward_backward_times(y, w, 10 ** rng.uniform(0, 3, T - d), t, d, np.zeros(T))
+    assert rel(o["z"], y) < 1e-10
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_times_exact_rational(d):
+    """Eq. (1) on rational uneven times minimised exactly == oracle."""
+    T = 8
+    times = [Fraction(int(v)) for v in _uneven_times(T, 1, 5)]
+    Drat = divided_difference_matrix(times, d)
+    y = dyadic(T, -2, 2)
+    w = [Fraction(int(b)) for b in (rng.random(T) < 0.6)]
+    for i in range(d):
+        w[2 * i] = Fraction(1)
+    lam = dyadic(T - d, 1, 20)
+
+    def obj(z):
+        dz = [sum(Drat[r][j] * z[j] for j in range(T)) for r in range(T - d)]
+        return sum(wi * (yi - zi) ** 2 for wi, yi, zi in zip(w, y, z)) + sum(l * v * v for l, v in zip(lam, dz))
+
+    zero = [Fraction(0)] * T
+    f0 = obj(zero)
+    fp = [obj([Fraction(int(i == j)) for j in range(T)]) for i in range(T)]
+    fm = [obj([Fraction(-int(i == j)) for j in range(T)]) for i in range(T)]
+    H = [[None] * T for _ in range(T)]
+    for i in range(T):
+        H[i][i] = fp[i] + fm[i] - 2 * f0
+        for j in range(i + 1, T):
+            H[i][j] = H[j][i] = obj([Fraction(int(k in (i, j))) for k in range(T)]) - fp[i] - fp[j] + f0
+    A = [row[:] + [-(fp[i] - fm[i]) / 2] for i, row in enumerate(H)]
+    for c in range(T):
+        p_ = next(r for r in range(c, T) if A[r][c] != 0)
+        A[c], A[p_] = A[p_], A[c]
+        A[c] = [x / A[c][c] for x in A[c]]
+        for r in range(T):
+            if r != c and A[r][c] != 0:
+                f = A[r][c]
+                A[r] = [a - f * b for a, b in zip(A[r], A[c])]
+    z_exact = [float(A[i][T]) for i in range(T)]
+    o = O1.forward_backward_times(np.array(y, float), np.array(w, float), np.array(lam, float),
+                                  np.array(times, float), d, np.zeros(T))
+    assert rel(o["z"], z_exact) < 1e-13
+
+
+def test_times_gradients_fd():
+    T, d = 30, 2
+    t = _uneven_times(T)
+    y, g = rng.normal(size=T), rng.normal(size=T)
+    w = (rng.random(T) < 0.6).astype(float)
+    w[:3] = 1
+    lam = 10 ** rng.uniform(0, 2, T - d)
+    o = O1.forward_backward_times(y, w, lam, t, d, g)
+
+    def L(lv):
+        return float(np.dot(g, O1.forward_backward_times(y, w, lv, t, d, np.zeros(T))["z"].astype(float)))
+
+    h = 1e-6
+    fd = np.array([(L(lam * np.exp(h * e)) - L(lam * np.exp(-h * e))) / (2 * h) for e in np.eye(T - d)]) / lam
+    assert rel(o["lambar"], fd) < 1e-6
