@@ -490,7 +490,7 @@ def run_s2tile(args, P, synth, dev, ws_n, rank):
     return 0
 
 
-def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=16384, nbuf=3):
+def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6):
     """Same metric through the public C-ABI with pinned HOST buffers: whit_run_host streams the
     batch in series chunks (pitched 2-D H2D copies of y, w, lambda, g; whit_forward +
     whit_backward; D2H of z, grad_y, grad_lambda), copies overlapping kernels on nbuf streams."""

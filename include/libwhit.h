@@ -178,6 +178,26 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
 whit_status whit_backward_bands(const void* grad_z, whit_ws* factor_ws, const void* z, void* grad_y,
                                 void* grad_lambda);
 
+/* ---------------------------------------------------------------------------
+ * Irregular acquisition grid (NEXT-2; the paper's formulation on uneven dates,
+ * P:26-28): D is the order-d dspline divided-difference operator on per-series
+ * times, row r: c_{r,j} = (d-1)! (t_{r+d} - t_r) / prod_{i != j} (t_{r+j} - t_{r+i})
+ * (plain differences for d = 1; the daily stencil on unit-spaced times).
+ *   times [T][B] (I/O dtype), strictly increasing per series (e.g. days; pad
+ *   unaligned series with w = 0 at increasing dummy dates).
+ * Workspace from whit_ws_create_times (checkpoint interval 8); the matching
+ * backward is whit_backward (the workspace remembers times, which must stay
+ * valid and unmodified until it has run).  info: T-d+1 (< d observed days),
+ * -1 (other non-positive pivot).  Single band.  One launch each. */
+size_t whit_ws_bytes_times(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode);
+
+whit_status whit_ws_create_times(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
+                                 whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes,
+                                 void* cuda_stream);
+
+whit_status whit_forward_times(const void* y, const void* w, const void* lambda, const void* times, int d,
+                               int64_t T, int64_t B, void* z, whit_ws* factor_ws);
+
 /* Forward fused with the training loss (NEXT-3): the paper trains with a
  * masking strategy and an MSE loss, the MSE of P:222:
  *     loss[b]   = T^{-1} sum_t loss_w[t][b] (z[t][b] - y[t][b])^2

@@ -43,6 +43,10 @@ SIGNATURES = [
                                             ctypes.c_int, _VP, _SZ, _VP]),
     ("whit_forward_bands", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, _VP, _VP]),
     ("whit_backward_bands", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("whit_ws_bytes_times", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int]),
+    ("whit_ws_create_times", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
+                                            _VP, _SZ, _VP]),
+    ("whit_forward_times", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_forward_mse", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP, _VP, _VP]),
     ("whit_posterior_variance", ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_host_ws_bytes", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -109,19 +113,28 @@ def whit_ws_bytes_bands(d: int, T: int, B: int, C: int, dtype: torch.dtype, per_
 
 
 class Workspace:
-    """Host handle (``whit_ws*``) plus the torch-owned device buffer it binds (C bands per pixel)."""
+    """Host handle (``whit_ws*``) plus the torch-owned device buffer it binds (C bands per pixel,
+    or an irregular-grid workspace with ``times=True``)."""
 
     def __init__(self, d: int, T: int, B: int, dtype: torch.dtype, per_date: bool, device=None, stream=None,
-                 C: int = 1):
-        nbytes = whit_ws_bytes_bands(d, T, B, C, dtype, per_date)
+                 C: int = 1, times: bool = False):
+        if times:
+            nbytes = int(_lib.whit_ws_bytes_times(d, T, B, _dtype_code(dtype), int(per_date)))
+        else:
+            nbytes = whit_ws_bytes_bands(d, T, B, C, dtype, per_date)
         if nbytes == 0:
-            raise WhitError(1, f"whit_ws_bytes_bands(d={d}, T={T}, B={B}, C={C})")
+            raise WhitError(1, f"workspace bytes(d={d}, T={T}, B={B}, C={C}, times={times})")
         self.d, self.T, self.B, self.C, self.dtype, self.per_date = d, T, B, C, dtype, per_date
         self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
         h = ctypes.c_void_p()
-        _check(_lib.whit_ws_create_bands(ctypes.byref(h), d, T, B, C, _dtype_code(dtype), int(per_date),
-                                         ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
-               "whit_ws_create_bands")
+        if times:
+            _check(_lib.whit_ws_create_times(ctypes.byref(h), d, T, B, _dtype_code(dtype), int(per_date),
+                                             ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
+                   "whit_ws_create_times")
+        else:
+            _check(_lib.whit_ws_create_bands(ctypes.byref(h), d, T, B, C, _dtype_code(dtype), int(per_date),
+                                             ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
+                   "whit_ws_create_bands")
         self.handle = h
 
     def set_stream(self, stream=None):
@@ -149,6 +162,11 @@ def whit_backward_bands(grad_z, ws: Workspace, z, grad_y, grad_lambda):
 
 def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):
     _check(_lib.whit_backward(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)), "whit_backward")
+
+
+def whit_forward_times(y, w, lam, times, d: int, T: int, B: int, z, ws: Workspace):
+    _check(_lib.whit_forward_times(_ptr(y), _ptr(w), _ptr(lam), _ptr(times), d, T, B, _ptr(z), ws.handle),
+           "whit_forward_times")
 
 
 def whit_forward_mse(y, w, lam, loss_w, d: int, T: int, B: int, z, grad_z, loss, ws: Workspace):

@@ -55,12 +55,13 @@ struct WsLayout {
 // Workspace of nb bands x B pixels: D z cache [nb][T-d][B] (I/O dtype), factor
 // checkpoints [C][NFAC][B] + forward / backward rhs checkpoints [C][nb][d][B]
 // (fp64), info[B], a failure counter.
-bool layout(int d, int64_t T, int64_t B, int nb, whit_dtype dt, WsLayout* L) {
+bool layout(int d, int64_t T, int64_t B, int nb, whit_dtype dt, WsLayout* L, int kk = 0) {
   if (d < 1 || d > 3 || T < d + 1 || B < 1 || nb < 1 || nb > whit::kMaxBands ||
       (dt != WHIT_F32 && dt != WHIT_F64))
     return false;
   const size_t esz = dt == WHIT_F32 ? 4 : 8;
-  const int64_t C = (T + chunk_k(d) - 1) / chunk_k(d);
+  if (kk == 0) kk = chunk_k(d);
+  const int64_t C = (T + kk - 1) / kk;
   const int nfac = d + d * (d - 1) / 2;
   size_t o = 0;
   L->off_dz = o;    o = align256(o + size_t(nb) * size_t(T - d) * size_t(B) * esz);
@@ -116,6 +117,9 @@ struct whit_ws {
   int d;
   int64_t T, B;
   int nb;      // bands per pixel sharing w, lambda (1 = independent series)
+  int kk;      // checkpoint interval / tile rows (chunk_k(d), or 8 on an irregular grid)
+  bool irr;    // irregular acquisition grid (NEXT-2): forward must be whit_forward_times
+  const void* times;
   whit_dtype dt;
   whit_lambda_mode lm;
   char* buf;
@@ -253,7 +257,7 @@ whit_status dispatch_var_d(int d, const Params& p, cudaStream_t s) {
 whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const void* w, const void* lam) {
   std::memset(p, 0, sizeof *p);
   const int d = ws->d;
-  const int kK = chunk_k(d);
+  const int kK = ws->kk;
   whit_status st;
   if ((st = encode_map(&p->tm_rhs, rhs, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
   if ((st = encode_map(&p->tm_w, w, ws->dt, ws->B, ws->T, kK)) != WHIT_OK) return st;
@@ -273,6 +277,43 @@ whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const voi
   p->C = int((ws->T + kK - 1) / kK);
   p->nb = ws->nb;
   return WHIT_OK;
+}
+
+// Irregular grid: maps with the IrrLayout tile heights (K = 8) and the times map (box K + 2d).
+template <int D, typename IO, bool PD, bool BWD>
+whit_status launch_irr(const Params& p, cudaStream_t s) {
+  using L = whit::IrrLayout<D, IO, PD, BWD>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(whit::whit_irr_kernel<D, IO, PD, BWD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  });
+  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  const long long per_cta = 32 * L::WARPS;
+  const long long grid = (p.B + per_cta - 1) / per_cta;
+  whit::whit_irr_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3((unsigned)per_cta), L::SMEM, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return WHIT_OK;
+}
+
+template <typename IO, bool PD, bool BWD>
+whit_status dispatch_irr_d(int d, const Params& p, cudaStream_t s) {
+  switch (d) {
+    case 1: return launch_irr<1, IO, PD, BWD>(p, s);
+    case 2: return launch_irr<2, IO, PD, BWD>(p, s);
+    case 3: return launch_irr<3, IO, PD, BWD>(p, s);
+  }
+  return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+}
+
+template <bool BWD>
+whit_status dispatch_irr(const whit_ws* ws, const Params& p) {
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  if (ws->dt == WHIT_F32)
+    return pd ? dispatch_irr_d<float, true, BWD>(ws->d, p, ws->stream) : dispatch_irr_d<float, false, BWD>(ws->d, p, ws->stream);
+  return pd ? dispatch_irr_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_irr_d<double, false, BWD>(ws->d, p, ws->stream);
 }
 
 }  // namespace
@@ -307,8 +348,29 @@ size_t whit_ws_bytes(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_
   return whit_ws_bytes_bands(d, T, B, 1, dtype, lambda_mode);
 }
 
+static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                             whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream, bool irr);
+
 whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
                                  whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream) {
+  return ws_create(out, d, T, B, C, dtype, lambda_mode, dev_buf, dev_bytes, cuda_stream, false);
+}
+
+size_t whit_ws_bytes_times(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode) {
+  WsLayout L;
+  if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE) return 0;
+  if (!layout(d, T, B, 1, dtype, &L, 8)) return 0;
+  return L.total;
+}
+
+whit_status whit_ws_create_times(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
+                                 whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream) {
+  return ws_create(out, d, T, B, 1, dtype, lambda_mode, dev_buf, dev_bytes, cuda_stream, true);
+}
+
+static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                             whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes, void* cuda_stream,
+                             bool irr) {
   if (!out) return fail(WHIT_ERR_ARG, "out is NULL");
   *out = nullptr;
   if (d < 1 || d > 3) return fail(WHIT_ERR_ARG, "d = %d not in {1,2,3}", d);
@@ -324,7 +386,7 @@ whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int
     return fail(WHIT_ERR_ALIGN, "B = %lld must be a multiple of %d (16-B row stride)", (long long)B,
                 dtype == WHIT_F32 ? 4 : 2);
   WsLayout L;
-  layout(d, T, B, C, dtype, &L);
+  layout(d, T, B, C, dtype, &L, irr ? 8 : 0);
   if (!dev_buf) return fail(WHIT_ERR_WS, "workspace buffer is NULL");
   if (reinterpret_cast<uintptr_t>(dev_buf) & 255u) return fail(WHIT_ERR_ALIGN, "workspace buffer not 256-B aligned");
   if (dev_bytes < L.total)
@@ -332,6 +394,7 @@ whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int
   whit_ws* ws = new (std::nothrow) whit_ws;
   if (!ws) return fail(WHIT_ERR_ARG, "host allocation failed");
   ws->d = d; ws->T = T; ws->B = B; ws->nb = C; ws->dt = dtype; ws->lm = lambda_mode;
+  ws->irr = irr; ws->kk = irr ? 8 : chunk_k(d); ws->times = nullptr;
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
@@ -360,6 +423,7 @@ void whit_ws_destroy(whit_ws* ws) { delete ws; }
 whit_status whit_forward_bands(const void* y, const void* w, const void* lambda, int d, int64_t T, int64_t B, int C,
                                void* z, whit_ws* ws) {
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (ws->irr) return fail(WHIT_ERR_STATE, "irregular-grid workspace: use whit_forward_times");
   if (!y || !w || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
   if (d != ws->d || T != ws->T || B != ws->B || C != ws->nb)
     return fail(WHIT_ERR_SHAPE, "(d,T,B,C) = (%d,%lld,%lld,%d) != workspace (%d,%lld,%lld,%d)", d, (long long)T,
@@ -383,11 +447,39 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   return WHIT_OK;
 }
 
+whit_status whit_forward_times(const void* y, const void* w, const void* lambda, const void* times, int d, int64_t T,
+                               int64_t B, void* z, whit_ws* ws) {
+  if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (!ws->irr) return fail(WHIT_ERR_STATE, "workspace not created by whit_ws_create_times");
+  if (!y || !w || !lambda || !times || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
+  if (d != ws->d || T != ws->T || B != ws->B)
+    return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
+                (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
+  if (!aligned16(y) || !aligned16(w) || !aligned16(lambda) || !aligned16(times) || !aligned16(z))
+    return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
+  if (z == y || z == w || z == lambda || z == times) return fail(WHIT_ERR_ARG, "z aliases an input");
+  DeviceGuard guard(ws->device);
+  if (!guard.ok) return fail(WHIT_ERR_CUDA, "cudaSetDevice(%d) failed", ws->device);
+  Params p;
+  whit_status st = fill_params(ws, &p, y, w, lambda);
+  if (st != WHIT_OK) return st;
+  const int kK = ws->kk;
+  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_lw, times, ws->dt, B, T, kK + 2 * d)) != WHIT_OK) return st;
+  ws->have_fwd = false;
+  st = dispatch_irr<false>(ws, p);
+  if (st != WHIT_OK) return st;
+  ws->have_fwd = true;
+  ws->w = w; ws->lam = lambda; ws->z = z; ws->times = times;
+  return WHIT_OK;
+}
+
 whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, const void* loss_w, int d, int64_t T,
                              int64_t B, void* z, void* grad_z, void* loss, whit_ws* ws) {
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!y || !w || !lambda || !loss_w || !z || !grad_z || !loss) return fail(WHIT_ERR_ARG, "NULL data pointer");
-  if (ws->nb != 1) return fail(WHIT_ERR_SHAPE, "the fused loss needs a single-band workspace");
+  if (ws->nb != 1 || ws->irr) return fail(WHIT_ERR_SHAPE, "the fused loss needs a single-band daily-grid workspace");
   if (d != ws->d || T != ws->T || B != ws->B)
     return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
                 (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
@@ -449,6 +541,10 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
   } else {
     p.out1 = grad_lambda;
   }
+  if (ws->irr) {
+    if ((st = encode_map(&p.tm_lw, ws->times, ws->dt, ws->B, ws->T, kK + 2 * ws->d)) != WHIT_OK) return st;
+    return dispatch_irr<true>(ws, p);
+  }
   return dispatch<true>(ws, p);
 }
 
@@ -460,7 +556,7 @@ whit_status whit_posterior_variance(const void* w, const void* lambda, int d, in
                                     whit_ws* ws) {
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!w || !lambda || !var) return fail(WHIT_ERR_ARG, "NULL data pointer");
-  if (ws->nb != 1) return fail(WHIT_ERR_SHAPE, "posterior variance needs a single-band workspace");
+  if (ws->nb != 1 || ws->irr) return fail(WHIT_ERR_SHAPE, "posterior variance needs a single-band daily-grid workspace");
   if (d != ws->d || T != ws->T || B != ws->B)
     return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
                 (long long)B, ws->d, (long long)ws->T, (long long)ws->B);

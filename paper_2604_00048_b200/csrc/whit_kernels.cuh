@@ -686,6 +686,371 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
   }
 }
 
+// ------------------------------------------------------------------ irregular grid (NEXT-2)
+// The paper's operator on uneven acquisition dates t_0 < ... < t_{T-1} (dspline
+// divided differences): row r of D has coefficients
+//   c_{r,j} = (d-1)! (t_{r+d} - t_r) / prod_{i != j} (t_{r+j} - t_{r+i}),   j = 0..d.
+// Deviation form with a column-dependent unit factor (R-18): column k of M~ is d_k / c_{k,0}
+// (normalised stencil mu_k[j] = c_{k,j} / c_{k,0}, mu_k[0] = 1) and Lambda~_k = lambda_k c_{k,0}^2,
+// so D^T Lambda D = M~ Lambda~ M~^T again and the recurrences of R-10 hold with M_j replaced by
+// M~[t][t-j] = mu_{t-j}[j] and M_{j-m} by M~[t-m][t-j] = mu_{t-j}[j-m].  Columns k < 0 and
+// k >= T-d (no difference row) use the binomial M (their Lambda~ is 0, any unit column works).
+template <int D> struct IState {
+  FState<D> f;
+  double mu[D][D];  // mu[i][j] = mu_{t-1-i}[j+1]
+};
+
+// Normalised stencil of column k (times tk[0..D] = t_k..t_{k+D}) and its c_{k,0}.
+template <int D, int NEWTON>
+__device__ __forceinline__ void col_stencil(const double (&tk)[D + 1], double (&mu)[D], double& c0) {
+  if (D == 1) {
+    mu[0] = -1.0;
+    c0 = -1.0;
+  } else if (D == 2) {
+    const double h1 = tk[1] - tk[0], h2 = tk[2] - tk[1];
+    const double r2 = rcp64<NEWTON>(h2);
+    mu[1] = h1 * r2;
+    mu[0] = -1.0 - mu[1];
+    c0 = rcp64<NEWTON>(h1);
+  } else {
+    double P[D + 1];
+#pragma unroll
+    for (int j = 0; j <= D; ++j) {
+      double p = 1.0;
+#pragma unroll
+      for (int i = 0; i <= D; ++i)
+        if (i != j) p *= (tk[j] - tk[i]);
+      P[j] = p;
+    }
+    const double rp0 = rcp64<NEWTON>(P[0]);
+#pragma unroll
+    for (int j = 1; j <= D; ++j) mu[j - 1] = P[0] * rcp64<NEWTON>(P[j]);
+    double fact = 1.0;
+#pragma unroll
+    for (int i = 2; i < D; ++i) fact *= i;
+    c0 = fact * (tk[D] - tk[0]) * rp0;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void binomial_col(double (&mu)[D]) {
+#pragma unroll
+  for (int j = 1; j <= D; ++j) mu[j - 1] = Mj(D, j);
+}
+
+template <int D, int NEWTON>
+__device__ __forceinline__ void ldl_step_irr(IState<D>& S, const double (&mu_t)[D], double w, double lam_t,
+                                             double b, double (&A)[D], double& Dt, double& idt, double& vt) {
+  FState<D>& s = S.f;
+  // Mt[j] = M~[t][t-j] = mu_{t-j}[j] = S.mu[j-1][j-1];  Mm(m, j) = M~[t-m][t-j] = S.mu[j-1][j-m-1]
+  double E[D + 1];
+  E[D] = 0.0;
+  A[D - 1] = (-S.mu[D - 1][D - 1] * s.dl[D - 1]) * s.id[D - 1];
+#pragma unroll
+  for (int m = D - 1; m >= 1; --m) {
+    double e = (-(S.mu[D - 1][D - 1] * s.lm[D - 1])) * s.ap[m - 1][D - m - 1];
+#pragma unroll
+    for (int j = D - 1; j >= m + 1; --j) {
+      const double a = s.ap[m - 1][j - m - 1];
+      e = fma(-(S.mu[j - 1][j - 1] * s.lm[j - 1]), a, e);
+      e = fma(-E[j], a, e);
+      e = fma(-S.mu[j - 1][j - m - 1], E[j], e);
+    }
+    E[m] = e;
+    A[m - 1] = fma(-S.mu[m - 1][m - 1], s.dl[m - 1], e) * s.id[m - 1];
+  }
+  double dl = w;
+#pragma unroll
+  for (int j = D - 1; j >= 1; --j) dl = fma(-S.mu[j - 1][j - 1], E[j], dl);
+#pragma unroll
+  for (int j = D; j >= 1; --j) {
+    const double inner = (j < D) ? fma(S.mu[j - 1][j - 1], s.lm[j - 1], E[j]) : S.mu[j - 1][j - 1] * s.lm[j - 1];
+    dl = fma(-A[j - 1], inner, dl);
+  }
+  Dt = lam_t + dl;
+  idt = rcp64<NEWTON>(Dt);
+  double v = b;
+#pragma unroll
+  for (int j = D; j >= 1; --j) {
+    v = fma(-S.mu[j - 1][j - 1], s.v[j - 1], v);
+    v = fma(-A[j - 1], s.v[j - 1], v);
+  }
+  vt = v;
+#pragma unroll
+  for (int i = D - 1; i >= 1; --i) {
+    s.dl[i] = s.dl[i - 1]; s.id[i] = s.id[i - 1]; s.lm[i] = s.lm[i - 1]; s.v[i] = s.v[i - 1];
+#pragma unroll
+    for (int k = 0; k < D; ++k) { s.ap[i][k] = s.ap[i - 1][k]; S.mu[i][k] = S.mu[i - 1][k]; }
+  }
+  s.dl[0] = dl; s.id[0] = idt; s.lm[0] = lam_t; s.v[0] = v;
+#pragma unroll
+  for (int k = 0; k < D; ++k) { s.ap[0][k] = A[k]; S.mu[0][k] = mu_t[k]; }
+}
+
+// Stage: rhs K rows, w K rows, times K+2D rows (t0-D .. t0+K+D-1), lambda (K / K+D rows), D z K rows.
+template <int D, typename IO, bool PD, bool BWD>
+struct IrrLayout {
+  static constexpr int K = 8, ST = 2, WARPS = 4;
+  static constexpr int ROW = 32 * (int)sizeof(IO);
+  static constexpr int OFF_RHS = 0;
+  static constexpr int OFF_W = K * ROW;
+  static constexpr int OFF_TT = 2 * K * ROW;
+  static constexpr int OFF_LAM = OFF_TT + (K + 2 * D) * ROW;
+  static constexpr int OFF_DZ = OFF_LAM + (PD ? (K + D) * ROW : 0);
+  static constexpr int STAGE = (OFF_DZ + (BWD ? K * ROW : 0) + 127) / 128 * 128;
+  static constexpr int OUT = K * ROW;
+  static constexpr int WARP_SMEM = ST * STAGE + 2 * OUT;
+  static constexpr int SMEM = WARPS * WARP_SMEM;
+  static constexpr uint32_t BYTES_UP = (2 * K + (K + 2 * D) + (PD ? K : 0)) * ROW;
+  static constexpr uint32_t BYTES_DN = (2 * K + (K + 2 * D) + (PD ? K + D : 0) + (BWD ? K : 0)) * ROW;
+};
+
+template <int D, typename IO, bool PD, bool BWD>
+__device__ __forceinline__ void issue_tile_irr(const Params& p, unsigned char* stage, uint64_t* bar, int i, int C,
+                                               int c0) {
+  using L = IrrLayout<D, IO, PD, BWD>;
+  const bool up = i < C;
+  const int c = up ? i : 2 * C - 1 - i;
+  const int t0 = c * L::K;
+  mbar_arrive_expect_tx(bar, up ? L::BYTES_UP : L::BYTES_DN);
+  tma_load_3d(stage + L::OFF_RHS, &p.tm_rhs, c0, t0, 0, bar);
+  tma_load_2d(stage + L::OFF_W, &p.tm_w, c0, t0, bar);
+  tma_load_2d(stage + L::OFF_TT, &p.tm_lw, c0, t0 - D, bar);  // times (tm_lw reused: box K+2D)
+  if (PD) {
+    if (up) tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_up, c0, t0, bar);
+    else tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_dn, c0, t0 - D, bar);
+  }
+  if (BWD && !up) tma_load_3d(stage + L::OFF_DZ, &p.tm_dz, c0, t0, 0, bar);
+}
+
+// mu and c0 of column k = t0 + kk (kk may be in [-D, K)), times tile row index kk + D.
+template <int D, typename IO, int NEWTON>
+__device__ __forceinline__ void tile_col(const IO* tt, int kk, int k, int T, double (&mu)[D], double& c0) {
+  if (k < 0 || k >= T - D) {
+    binomial_col<D>(mu);
+    c0 = 0.0;
+    return;
+  }
+  double tk[D + 1];
+#pragma unroll
+  for (int j = 0; j <= D; ++j) tk[j] = to_f64<IO>(tt[(kk + D + j) * 32]);
+  col_stencil<D, NEWTON>(tk, mu, c0);
+}
+
+template <int D, typename IO, bool PD, bool BWD>
+__global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params p) {
+  using L = IrrLayout<D, IO, PD, BWD>;
+  constexpr int K = L::K, ST = L::ST, WARPS = L::WARPS;
+  constexpr int NFAC = Ck<D>::NFAC;
+  constexpr int NW = Newton<IO>::N;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[WARPS][ST];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = p.T, C = p.C, TmD = T - D;
+  const long long B = p.B;
+  const long long bw = ((long long)blockIdx.x * WARPS + warp) * 32;
+  if (bw >= B) return;
+  const long long b = bw + lane;
+  const bool valid = b < B;
+  unsigned char* ring = smem + warp * L::WARP_SMEM;
+  IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);
+  IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
+  uint64_t* bars = full_bar[warp];
+  const int ntiles = 2 * C;
+  if (lane == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < ST && i < ntiles; ++i)
+      issue_tile_irr<D, IO, PD, BWD>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw);
+  }
+  __syncwarp();
+  const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
+  double* const ck_rhs = (BWD ? p.ck_rhs_b : p.ck_rhs_f) + b;
+
+  IState<D> S;
+  state_init<D>(S.f);
+#pragma unroll
+  for (int i = 0; i < D; ++i) binomial_col<D>(S.mu[i]);
+  int nobs = 0;
+  bool allpos = true;
+  int it = 0;
+  // ================================================================ up sweep
+  for (int c = 0; c < C; ++c, ++it) {
+    const int s = it % ST;
+    mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
+    const unsigned char* stg = ring + s * L::STAGE;
+    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
+    const IO* t_tt = reinterpret_cast<const IO*>(stg + L::OFF_TT) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;
+    const int t0 = c * K;
+    if (valid) {
+      if (!BWD) {
+        double* ck = p.ck_fac + (long long)c * NFAC * B + b;
+        int f = 0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) ck[(long long)(f++) * B] = S.f.dl[i];
+#pragma unroll
+        for (int m = 0; m < D - 1; ++m)
+#pragma unroll
+          for (int k = 0; k < D - 1 - m; ++k) ck[(long long)(f++) * B] = S.f.ap[m][k];
+      }
+      double* ck = ck_rhs + (long long)c * D * B;
+#pragma unroll
+      for (int i = 0; i < D; ++i) ck[(long long)i * B] = S.f.v[i];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int t = t0 + k;
+      if (t >= T) break;
+      const IO wio = t_w[k * 32];
+      const double w = to_f64<IO>(wio);
+      double mu_t[D], c0;
+      tile_col<D, IO, NW>(t_tt, k, t, T, mu_t, c0);
+      const double lraw = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
+      const double lt = (t < TmD) ? lraw * c0 * c0 : 0.0;  // Lambda~_t = lambda_t c_{t,0}^2
+      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+      double A[D], Dt, idt, vt;
+      ldl_step_irr<D, NW>(S, mu_t, w, lt, bb, A, Dt, idt, vt);
+      if (!BWD) {
+        nobs += (wio > IO(0));
+        allpos = allpos && (Dt > 0.0);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && it + ST < ntiles) {
+      fence_proxy_async_smem();
+      issue_tile_irr<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw);
+    }
+  }
+  bool failed;
+  if (!BWD) {
+    if (valid) p.info[b] = (nobs < D) ? (T - D + 1) : (allpos ? 0 : -1);
+    failed = (nobs < D) || !allpos;
+  } else {
+    failed = valid ? (p.info[b] != 0) : true;
+  }
+  const double poison = failed ? qnan() : 0.0;
+
+  // ================================================================ down sweep
+  double cA[D][D], cM[D][D];  // A[t0+K+i][j+1] and mu_{t0+K+i}[j+1] of the later chunk
+  double zw[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    zw[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) { cA[i][j] = 0.0; cM[i][j] = Mj(D, j + 1); }
+  }
+  double lam_acc = 0.0;
+  for (int c = C - 1; c >= 0; --c, ++it) {
+    const int s = it % ST;
+    mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
+    const unsigned char* stg = ring + s * L::STAGE;
+    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
+    const IO* t_tt = reinterpret_cast<const IO*>(stg + L::OFF_TT) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
+    const IO* t_dz = reinterpret_cast<const IO*>(stg + L::OFF_DZ) + lane;
+    const int t0 = c * K;
+    // restore the state entering row t0
+    if (valid) {
+      const double* ckf = p.ck_fac + (long long)c * NFAC * B + b;
+      int f = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) S.f.dl[i] = ckf[(long long)(f++) * B];
+#pragma unroll
+      for (int m = 0; m < D - 1; ++m)
+#pragma unroll
+        for (int k = 0; k < D - 1 - m; ++k) S.f.ap[m][k] = ckf[(long long)(f++) * B];
+      const double* ckr = ck_rhs + (long long)c * D * B;
+#pragma unroll
+      for (int i = 0; i < D; ++i) S.f.v[i] = ckr[(long long)i * B] + poison;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int tj = t0 - 1 - i;
+      double c0;
+      tile_col<D, IO, NW>(t_tt, -1 - i, tj, T, S.mu[i], c0);
+      const double lraw = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : lam_s;
+      const double l = (tj >= 0 && tj < TmD) ? lraw * c0 * c0 : 0.0;
+      S.f.lm[i] = l;
+      S.f.id[i] = (tj < 0) ? 1.0 : rcp64<NW>(l + S.f.dl[i]);
+    }
+    double q[K], Ak[K][D], Mk[K][D], c0k[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int t = t0 + k;
+      const IO wio = t_w[k * 32];
+      const double w = to_f64<IO>(wio);
+      double c0;
+      tile_col<D, IO, NW>(t_tt, k, t, T, Mk[k], c0);
+      c0k[k] = c0;
+      const double lraw = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
+      const double lt = (t < TmD) ? lraw * c0 * c0 : 0.0;
+      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+      double Dt, idt, vt;
+      ldl_step_irr<D, NW>(S, Mk[k], w, lt, bb, Ak[k], Dt, idt, vt);
+      q[k] = vt * idt;
+      if (t >= T) {
+        q[k] = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) Ak[k][j] = 0.0;
+      }
+    }
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
+#pragma unroll
+    for (int k = K - 1; k >= 0; --k) {
+      const int t = t0 + k;
+      double z = q[k];
+      // z_t = q_t - sum_j (M~[t+j][t] + A[t+j][j]) z_{t+j},  M~[t+j][t] = mu_t[j]
+#pragma unroll
+      for (int j = D; j >= 1; --j) {
+        const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
+        z = fma(-Mk[k][j - 1], zw[j - 1], z);
+        z = fma(-a, zw[j - 1], z);
+      }
+      // (D z)_t = c_{t,0} (z_t + sum_j mu_t[j] z_{t+j})
+      double u = z;
+#pragma unroll
+      for (int j = 1; j <= D; ++j) u = fma(Mk[k][j - 1], zw[j - 1], u);
+      const double dz = c0k[k] * u;
+#pragma unroll
+      for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
+      zw[0] = z;
+      if (!BWD) {
+        so0[k * 32 + lane] = from_f64<IO>(z);
+        so1[k * 32 + lane] = from_f64<IO>(dz);
+      } else {
+        const double w = to_f64<IO>(t_w[k * 32]);
+        so0[k * 32 + lane] = from_f64<IO>(w * z);
+        const double g = -dz * to_f64<IO>(t_dz[k * 32]);
+        if (PD) so1[k * 32 + lane] = from_f64<IO>(g);
+        else if (t < TmD) lam_acc += g;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) { cA[i][j] = Ak[i][j]; cM[i][j] = Mk[i][j]; }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(&p.tm_out0, so0, (int)bw, t0, 0);
+      if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, 0);
+      if (BWD && PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
+      bulk_commit();
+      if (it + ST < ntiles) {
+        fence_proxy_async_smem();
+        issue_tile_irr<D, IO, PD, BWD>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) bulk_wait0();
+  if (BWD && !PD && valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc);
+}
+
 // ------------------------------------------------------------------ posterior variance (NEXT-4)
 // diag(Omega^{-1}) by Takahashi's selected inversion on the same deviation-form
 // factor (R-15).  With Sigma = Omega^{-1} = L^{-T} D^{-1} L^{-1}, rows descending:

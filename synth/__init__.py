@@ -243,3 +243,17 @@ def make_inputs_bands(cfg: Config | str, C: int, *, B: int | None = None, T: int
             g[c, t0:t1] = _normal(S.per_cell(102 + 4 * c, t), S.per_cell(103 + 4 * c, t)).to(dtype)
     return {"y": y, "w": base["w"].to(dtype), "lam": base["lam"].to(dtype), "g": g, "B": B, "T": T, "d": d, "C": C,
             "lam_mode": base["lam_mode"], "seed": base["seed"], "series_offset": series_offset}
+
+
+def make_times(B: int, T: int, *, seed: int = BASE_SEED + 7, series_offset: int = 0, device="cpu",
+               dtype=torch.float32, max_gap: int = 12) -> torch.Tensor:
+    """Per-series increasing acquisition days [T][B] for the irregular-grid path: cumulative
+    gaps uniform in {1..max_gap} (Sentinel-2 revisits are 5-10 days; unaligned series,
+    P:26), first date in [0, 10)."""
+    dev = torch.device(device)
+    ser = torch.arange(series_offset, series_offset + B, dtype=torch.int64, device=dev)
+    S = _Stream(seed, ser)
+    t = torch.arange(T, dtype=torch.int64, device=dev)[:, None]
+    gaps = 1 + torch.floor(S.per_cell(60, t) * max_gap)
+    gaps[0] = torch.floor(S.per_series(61) * 10)
+    return torch.cumsum(gaps, dim=0).to(dtype)

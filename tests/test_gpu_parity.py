@@ -407,3 +407,54 @@ def test_fused_mse_forward(dtype, per_date):
         assert rel_series(gz[:, b].double().cpu().numpy(), g1).max() <= tg
         o = O1.backward(g1.astype(float), h["w"][b], h["lam"][b], d, z1)
         assert rel_series(gy[:, b].double().cpu().numpy(), o[0]).max() <= tg
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_irregular_grid_vs_oracle(d, per_date, dtype):
+    """NEXT-2: uneven per-series acquisition dates (dspline divided differences) through
+    whit_forward_times + whit_backward vs the oracle's dense definition on the same grid."""
+    import paper_2604_00048_b200 as P
+
+    T, B = 203, 132
+    x = synth.make_inputs("toy", B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", dtype=dtype, seed=40 + d)
+    tt = synth.make_times(B, T, device="cuda", dtype=dtype)
+    y, w, lam, g = (x[k].contiguous() for k in ("y", "w", "lam", "g"))
+    ws = P.Workspace(d, T, B, dtype, per_date, times=True)
+    z, gy, gl = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam)
+    P.whit_forward_times(y, w, lam, tt, d, T, B, z, ws)
+    P.whit_backward(g, ws, z, gy, gl)
+    torch.cuda.synchronize()
+    h = host_inputs(x)
+    th = tt.double().cpu().numpy().T
+    tz, tg = TOL[(dtype, d)]
+    if d == 3 and dtype == torch.float32:
+        tz, tg = 1e-3, 1e-2
+    for b in range(0, B, 5):
+        o = O1.forward_backward_times(h["y"][b], h["w"][b], h["lam"][b], th[b], d, h["g"][b])
+        ez = np.max(np.abs(z[:, b].double().cpu().numpy() - o["z"].astype(float))) / ymax_observed(h["y"][b], h["w"][b])
+        assert ez <= tz, (b, ez)
+        assert rel_series(gy[:, b].double().cpu().numpy(), o["ybar"]).max() <= tg, b
+        got = gl[:, b].double().cpu().numpy() if per_date else gl[b].item()
+        if per_date:
+            assert rel_series(got, o["lambar"]).max() <= tg, b
+        else:
+            terms = -(O1.difference_matrix_times(th[b], d) @ o["u"]) * o["dz"]
+            assert abs(got - float(o["lambar"])) / np.sum(np.abs(terms.astype(float))) <= tg, b
+
+
+def test_irregular_unit_spacing_equals_daily_path():
+    """Unit-spaced times reproduce the daily-grid kernels' results (to rounding)."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 150, 64
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64, seed=3)
+    tt = (torch.arange(T, dtype=torch.float64, device="cuda")[:, None] + 100.0).expand(T, B).contiguous()
+    ws = P.Workspace(d, T, B, torch.float64, True, times=True)
+    z = torch.empty_like(x["y"])
+    P.whit_forward_times(x["y"], x["w"], x["lam"], tt, d, T, B, z, ws)
+    ref = run_cuda(x, d, torch.float64, backward=False)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(z.cpu().numpy().T - ref["z"])) <= 1e-12 * np.max(np.abs(ref["z"]))
