@@ -436,7 +436,7 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   Params p;
   whit_status st = fill_params(ws, &p, y, w, lambda);
   if (st != WHIT_OK) return st;
-  const int kK = chunk_k(d);
+  const int kK = ws->kk;
   if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
   if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
   ws->have_fwd = false;
@@ -494,7 +494,7 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
   Params p;
   whit_status st = fill_params(ws, &p, y, w, lambda);
   if (st != WHIT_OK) return st;
-  const int kK = chunk_k(d);
+  const int kK = ws->kk;
   if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
   if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
   if ((st = encode_map(&p.tm_lw, loss_w, ws->dt, B, T, kK)) != WHIT_OK) return st;
@@ -532,7 +532,7 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
   Params p;
   whit_status st = fill_params(ws, &p, grad_z, ws->w, ws->lam);
   if (st != WHIT_OK) return st;
-  const int kK = chunk_k(ws->d);
+  const int kK = ws->kk;
   if ((st = encode_map(&p.tm_dz, ws->buf + ws->L.off_dz, ws->dt, ws->B, ws->T - ws->d, kK, ws->nb)) != WHIT_OK)
     return st;
   if ((st = encode_map(&p.tm_out0, grad_y, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
@@ -568,7 +568,7 @@ whit_status whit_posterior_variance(const void* w, const void* lambda, int d, in
   Params p;
   whit_status st = fill_params(ws, &p, w /* unused rhs slot */, w, lambda);
   if (st != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out0, var, ws->dt, B, T, chunk_k(d), 1)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out0, var, ws->dt, B, T, ws->kk, 1)) != WHIT_OK) return st;
   // the factor checkpoints are shared with the forward: a different (w, lambda) invalidates its backward
   if (w != ws->w || lambda != ws->lam) ws->have_fwd = false;
   const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
