@@ -176,6 +176,8 @@ whit_status launch(const Params& p, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
+    cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
     attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
   });
@@ -231,6 +233,8 @@ whit_status launch_var(const Params& p, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
+    cudaFuncSetAttribute(whit::whit_var_kernel<D, IO, PD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
     attr_err = cudaFuncSetAttribute(whit::whit_var_kernel<D, IO, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     V::SMEM);
   });
@@ -286,6 +290,8 @@ whit_status launch_irr(const Params& p, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
+    cudaFuncSetAttribute(whit::whit_irr_kernel<D, IO, PD, BWD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
     attr_err = cudaFuncSetAttribute(whit::whit_irr_kernel<D, IO, PD, BWD>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
   });

@@ -260,17 +260,18 @@ template <int D> struct Ck {
 // One warp = 32 series = one TMA pipeline.  K time steps per chunk/tile, ST
 // ring stages per warp, WARPS warps per CTA.  K = 16 for d <= 2; d = 3 keeps
 // 4 fp64 values per chunk row in registers, so its chunk is 8 steps.
-// Registers are granted to a CTA in units of 4 warps (cudaFuncGetAttributes:
-// maxThreadsPerBlock = 256 at 192 regs, 384 at 168).  Forward: 4-warp CTAs, 3 per SM
-// (12 warps, <= 168 regs, 16.8 KB smem per warp).  Backward (one more staged
-// input plane, 21 KB per warp): 2-warp CTAs, 5 per SM (10 warps, <= 200 regs).
+// Registers are granted per SMSP file (16K regs each; cudaFuncGetAttributes:
+// maxThreadsPerBlock = 256 at 192 regs, 384 at 168), so 12 warps/SM need <= 168
+// regs.  Forward: 4-warp CTAs, 3 per SM (16.8 KB smem per warp).  Backward: its
+// outputs are staged IN PLACE in the consumed g / D z slots of the stage (16.9
+// KB per warp), 2-warp CTAs, 6 per SM (12 warps).
 // Multi-band (MB): one CTA = nb warps (one band each) over the same 32 pixels,
 // <= 168 regs so that up to 12 warps fit one CTA.
 template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int K = D <= 2 ? 16 : 8;
   static constexpr int ST = 2;
   static constexpr int WARPS = BWD ? 2 : 4;
-  static constexpr int MAXREG = BWD ? 200 : 168;
+  static constexpr int MAXREG = 168;  // registers live in the 4 SMSP files (16K each): 3 warps/SMSP at <= 168
   static constexpr int MB_MAXREG = 168;  // registers are granted per 4 warps: 12 x 32 x 168 <= 64K
 };
 constexpr int kMaxBands = 10;
@@ -285,7 +286,9 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false> struct Layou
   static constexpr int OFF_LW = OFF_DZ + (BWD ? K * ROW : 0);  // LOSS (forward): loss-weight tile
   static constexpr int STAGE = (OFF_LW + (LOSS ? K * ROW : 0) + 127) / 128 * 128;
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
-  static constexpr int WARP_SMEM = ST * STAGE + (LOSS ? 3 : 2) * OUT;  // ring + out0 + out1 (+ out2)
+  // backward: grad_y staged in the stage's g slot, grad_lambda in its D z slot (both consumed)
+  static constexpr bool INPLACE = BWD;
+  static constexpr int WARP_SMEM = ST * STAGE + (INPLACE ? 0 : (LOSS ? 3 : 2) * OUT);  // ring (+ out0, out1, out2)
   static constexpr int SMEM = WARPS * WARP_SMEM;
   // multi-band CTA of nb warps: rings + reduction tile + scalar slots
   static constexpr int smem_mb(int nb) { return nb * WARP_SMEM + OUT + nb * 32 * 8; }
@@ -495,7 +498,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
   const long long b = bw + lane;
   const bool valid = b < B;
   unsigned char* ring = smem + warp * L::WARP_SMEM;
-  IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);
+  IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);             // forward staging (not INPLACE)
   IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
   IO* so2 = reinterpret_cast<IO*>(ring + ST * L::STAGE + 2 * L::OUT);  // LOSS only
   uint64_t* bars = full_bar[warp];
@@ -626,8 +629,13 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     if (c > 0) WHIT_LOAD_CK(c - 1);
 
     // the staging tiles must have been read by the previous chunk's TMA stores
-    if (lane == 0) bulk_wait_read0();
-    __syncwarp();
+    if (!L::INPLACE) {
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+    } else {
+      so0 = reinterpret_cast<IO*>(const_cast<unsigned char*>(stg) + L::OFF_RHS);
+      so1 = reinterpret_cast<IO*>(const_cast<unsigned char*>(stg) + L::OFF_DZ);
+    }
     const double two_over_T = 2.0 / (double)T;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
@@ -651,7 +659,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
       for (int k = warp; k < K; k += nb) {
         double acc = 0.0;
         for (int cb = 0; cb < nb; ++cb)
-          acc += to_f64<IO>(reinterpret_cast<const IO*>(smem + cb * L::WARP_SMEM + ST * L::STAGE + L::OUT)[k * 32 + lane]);
+          acc += to_f64<IO>(reinterpret_cast<const IO*>(smem + cb * L::WARP_SMEM + s * L::STAGE + L::OFF_DZ)[k * 32 + lane]);
         red[k * 32 + lane] = from_f64<IO>(acc);
       }
       fence_proxy_async_smem();
@@ -664,6 +672,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
 
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
+      if (L::INPLACE) bulk_wait_read0();  // the stores read this very stage
       fence_proxy_async_smem();
       issue_tile<D, IO, PD, BWD, LOSS>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }
