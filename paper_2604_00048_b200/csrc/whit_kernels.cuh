@@ -262,16 +262,17 @@ template <int D> struct Ck {
 // 4 fp64 values per chunk row in registers, so its chunk is 8 steps.
 // Registers are granted per SMSP file (16K regs each; cudaFuncGetAttributes:
 // maxThreadsPerBlock = 256 at 192 regs, 384 at 168), so 12 warps/SM need <= 168
-// regs.  Forward: 4-warp CTAs, 3 per SM (16.8 KB smem per warp).  Backward: its
-// outputs are staged IN PLACE in the consumed g / D z slots of the stage (16.9
-// KB per warp), 2-warp CTAs, 6 per SM (12 warps).
+// regs.  Forward: 4-warp CTAs, 3 per SM (16.8 KB smem per warp).  Backward (one
+// more staged plane, 21 KB per warp): 2-warp CTAs at <= 200 regs (8 warps/SM);
+// ncu shows both DRAM-bound (~6.0 TB/s), and staging the backward's outputs in
+// place to reach 12 warps measured no faster (slower on small batches).
 // Multi-band (MB): one CTA = nb warps (one band each) over the same 32 pixels,
 // <= 168 regs so that up to 12 warps fit one CTA.
 template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int K = D <= 2 ? 16 : 8;
   static constexpr int ST = 2;
   static constexpr int WARPS = BWD ? 2 : 4;
-  static constexpr int MAXREG = 168;  // registers live in the 4 SMSP files (16K each): 3 warps/SMSP at <= 168
+  static constexpr int MAXREG = BWD ? 200 : 168;  // SMSP register files (16K): 3 warps/SMSP need <= 168
   static constexpr int MB_MAXREG = 168;  // registers are granted per 4 warps: 12 x 32 x 168 <= 64K
 };
 constexpr int kMaxBands = 10;
@@ -287,7 +288,7 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false> struct Layou
   static constexpr int STAGE = (OFF_LW + (LOSS ? K * ROW : 0) + 127) / 128 * 128;
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
   // backward: grad_y staged in the stage's g slot, grad_lambda in its D z slot (both consumed)
-  static constexpr bool INPLACE = BWD;
+  static constexpr bool INPLACE = false;  // in-place backward staging measured slower (both kernels DRAM-bound)
   static constexpr int WARP_SMEM = ST * STAGE + (INPLACE ? 0 : (LOSS ? 3 : 2) * OUT);  // ring (+ out0, out1, out2)
   static constexpr int SMEM = WARPS * WARP_SMEM;
   // multi-band CTA of nb warps: rings + reduction tile + scalar slots

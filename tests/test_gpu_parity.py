@@ -319,7 +319,10 @@ def test_bands_one_equals_single_series_path():
 
 
 def test_bands_limits():
+    """C is capped at 10 (f32) / 5 (f64): one CTA's shared memory holds the C band pipelines."""
     import paper_2604_00048_b200 as P
+    P.Workspace(2, 100, 128, torch.float32, True, C=10)
+    P.Workspace(2, 100, 128, torch.float64, True, C=5)
     with pytest.raises(P.WhitError):
         P.Workspace(2, 100, 128, torch.float32, True, C=11)
     with pytest.raises(P.WhitError):
