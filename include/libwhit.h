@@ -198,6 +198,23 @@ whit_status whit_ws_create_times(whit_ws** out, int d, int64_t T, int64_t B, whi
 whit_status whit_forward_times(const void* y, const void* w, const void* lambda, const void* times, int d,
                                int64_t T, int64_t B, void* z, whit_ws* factor_ws);
 
+/* ---------------------------------------------------------------------------
+ * Bit-packed W.  The paper's W is binary (w_ii is 1 if the date was
+ * observed and not cloud-flagged, else 0); storing it as 1 bit per date
+ * instead of a float plane removes ~4 of the ~19 bytes per series-date each
+ * sweep reads.  Layout: uint32 [ceil(T/32)][B], bit j of word r of series b is
+ * (w[32r + j][b] != 0); bits past T are 0.  Results are bitwise identical to
+ * whit_forward / whit_backward with the 0/1 float plane.
+ *   whit_pack_mask   packs a [T][B] plane (any nonzero -> 1) on `cuda_stream`.
+ *   whit_forward_wbits  forward from the bits; the matching backward is
+ *                    whit_backward (the workspace remembers wbits, which must
+ *                    stay valid and unmodified until it has run).
+ * Single-band daily-grid workspaces (whit_ws_create). */
+whit_status whit_pack_mask(const void* w, int64_t T, int64_t B, whit_dtype dtype, uint32_t* bits, void* cuda_stream);
+
+whit_status whit_forward_wbits(const void* y, const uint32_t* wbits, const void* lambda, int d, int64_t T, int64_t B,
+                               void* z, whit_ws* factor_ws);
+
 /* Forward fused with the training loss (NEXT-3): the paper trains with a
  * masking strategy and an MSE loss, the MSE of P:222:
  *     loss[b]   = T^{-1} sum_t loss_w[t][b] (z[t][b] - y[t][b])^2

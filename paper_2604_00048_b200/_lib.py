@@ -47,6 +47,8 @@ SIGNATURES = [
     ("whit_ws_create_times", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                             _VP, _SZ, _VP]),
     ("whit_forward_times", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
+    ("whit_pack_mask", ctypes.c_int, [_VP, _I64, _I64, ctypes.c_int, _VP, _VP]),
+    ("whit_forward_wbits", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_forward_mse", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP, _VP, _VP]),
     ("whit_posterior_variance", ctypes.c_int, [_VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_host_ws_bytes", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -167,6 +169,19 @@ def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):
 def whit_forward_times(y, w, lam, times, d: int, T: int, B: int, z, ws: Workspace):
     _check(_lib.whit_forward_times(_ptr(y), _ptr(w), _ptr(lam), _ptr(times), d, T, B, _ptr(z), ws.handle),
            "whit_forward_times")
+
+
+def whit_pack_mask(w, bits=None, stream=None):
+    """Pack a 0/1 [T][B] weight plane into uint32 bits [ceil(T/32)][B] (as int32 tensor storage)."""
+    T, B = w.shape
+    if bits is None:
+        bits = torch.empty(((T + 31) // 32, B), dtype=torch.int32, device=w.device)
+    _check(_lib.whit_pack_mask(_ptr(w), T, B, _dtype_code(w.dtype), _ptr(bits), _stream_handle(stream)), "whit_pack_mask")
+    return bits
+
+
+def whit_forward_wbits(y, wbits, lam, d: int, T: int, B: int, z, ws: Workspace):
+    _check(_lib.whit_forward_wbits(_ptr(y), _ptr(wbits), _ptr(lam), d, T, B, _ptr(z), ws.handle), "whit_forward_wbits")
 
 
 def whit_forward_mse(y, w, lam, loss_w, d: int, T: int, B: int, z, grad_z, loss, ws: Workspace):

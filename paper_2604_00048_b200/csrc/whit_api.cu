@@ -120,6 +120,7 @@ struct whit_ws {
   int kk;      // checkpoint interval / tile rows (chunk_k(d), or 8 on an irregular grid)
   bool irr;    // irregular acquisition grid (NEXT-2): forward must be whit_forward_times
   const void* times;
+  const uint32_t* wbits;  // bit-packed W of the last forward (whit_forward_wbits), else NULL
   whit_dtype dt;
   whit_lambda_mode lm;
   char* buf;
@@ -168,17 +169,17 @@ constexpr int max_bands_io() {
 }
 int max_bands(whit_dtype dt) { return dt == WHIT_F32 ? max_bands_io<float>() : max_bands_io<double>(); }
 
-template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false>
+template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false, bool WB = false>
 whit_status launch(const Params& p, cudaStream_t s) {
-  using L = whit::Layout<D, IO, PD, BWD, LOSS>;
+  using L = whit::Layout<D, IO, PD, BWD, LOSS, WB>;
   constexpr int max_smem = MB ? L::smem_mb(max_bands_io<IO>()) : L::SMEM;
   static_assert(max_smem <= kSmemBudget, "CTA shared memory over budget");
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS, WB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS>,
+    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS, WB>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
   });
   if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
@@ -187,7 +188,7 @@ whit_status launch(const Params& p, cudaStream_t s) {
   const long long per_cta = MB ? 32 : threads;
   const long long grid = (p.B + per_cta - 1) / per_cta;
   const int smem = MB ? L::smem_mb(p.nb) : L::SMEM;
-  whit::whit_kernel<D, IO, PD, BWD, MB, LOSS><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
+  whit::whit_kernel<D, IO, PD, BWD, MB, LOSS, WB><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
@@ -207,6 +208,24 @@ template <typename IO, bool BWD, bool MB>
 whit_status dispatch_pd(const whit_ws* ws, const Params& p) {
   return ws->lm == WHIT_LAMBDA_PER_DATE ? dispatch_d<IO, true, BWD, MB>(ws->d, p, ws->stream)
                                         : dispatch_d<IO, false, BWD, MB>(ws->d, p, ws->stream);
+}
+
+template <typename IO, bool PD, bool BWD>
+whit_status dispatch_wb_d(int d, const Params& p, cudaStream_t s) {
+  switch (d) {
+    case 1: return launch<1, IO, PD, BWD, false, false, true>(p, s);
+    case 2: return launch<2, IO, PD, BWD, false, false, true>(p, s);
+    case 3: return launch<3, IO, PD, BWD, false, false, true>(p, s);
+  }
+  return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+}
+
+template <bool BWD>
+whit_status dispatch_wb(const whit_ws* ws, const Params& p) {
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  if (ws->dt == WHIT_F32)
+    return pd ? dispatch_wb_d<float, true, BWD>(ws->d, p, ws->stream) : dispatch_wb_d<float, false, BWD>(ws->d, p, ws->stream);
+  return pd ? dispatch_wb_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_wb_d<double, false, BWD>(ws->d, p, ws->stream);
 }
 
 template <bool BWD>
@@ -400,7 +419,7 @@ static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, 
   whit_ws* ws = new (std::nothrow) whit_ws;
   if (!ws) return fail(WHIT_ERR_ARG, "host allocation failed");
   ws->d = d; ws->T = T; ws->B = B; ws->nb = C; ws->dt = dtype; ws->lm = lambda_mode;
-  ws->irr = irr; ws->kk = irr ? 8 : chunk_k(d); ws->times = nullptr;
+  ws->irr = irr; ws->kk = irr ? 8 : chunk_k(d); ws->times = nullptr; ws->wbits = nullptr;
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
@@ -449,7 +468,52 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   st = dispatch<false>(ws, p);
   if (st != WHIT_OK) return st;
   ws->have_fwd = true;
-  ws->w = w; ws->lam = lambda; ws->z = z;
+  ws->w = w; ws->lam = lambda; ws->z = z; ws->wbits = nullptr;
+  return WHIT_OK;
+}
+
+whit_status whit_forward_wbits(const void* y, const uint32_t* wbits, const void* lambda, int d, int64_t T, int64_t B,
+                               void* z, whit_ws* ws) {
+  if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (ws->irr || ws->nb != 1) return fail(WHIT_ERR_STATE, "bit-packed W needs a single-band daily-grid workspace");
+  if (!y || !wbits || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
+  if (d != ws->d || T != ws->T || B != ws->B)
+    return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
+                (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
+  if (!aligned16(y) || !aligned16(wbits) || !aligned16(lambda) || !aligned16(z))
+    return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
+  if (z == y || z == (const void*)wbits || z == lambda) return fail(WHIT_ERR_ARG, "z aliases an input");
+  DeviceGuard guard(ws->device);
+  if (!guard.ok) return fail(WHIT_ERR_CUDA, "cudaSetDevice(%d) failed", ws->device);
+  Params p;
+  whit_status st = fill_params(ws, &p, y, y /* w map unused */, lambda);
+  if (st != WHIT_OK) return st;
+  p.wbits = wbits;
+  const int kK = ws->kk;
+  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
+  ws->have_fwd = false;
+  st = dispatch_wb<false>(ws, p);
+  if (st != WHIT_OK) return st;
+  ws->have_fwd = true;
+  ws->w = wbits; ws->lam = lambda; ws->z = z; ws->wbits = wbits;
+  return WHIT_OK;
+}
+
+whit_status whit_pack_mask(const void* w, int64_t T, int64_t B, whit_dtype dtype, uint32_t* bits, void* cuda_stream) {
+  if (!w || !bits) return fail(WHIT_ERR_ARG, "NULL pointer");
+  if (dtype != WHIT_F32 && dtype != WHIT_F64) return fail(WHIT_ERR_ARG, "bad dtype");
+  if (T < 1 || B < 1) return fail(WHIT_ERR_SHAPE, "bad T / B");
+  const long long rows = (T + 31) / 32;
+  if (rows > 65535) return fail(WHIT_ERR_SHAPE, "T too large for the packing grid");
+  cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+  dim3 grid((unsigned)((B + 255) / 256), (unsigned)rows);
+  if (dtype == WHIT_F32)
+    whit::pack_mask<float><<<grid, 256, 0, s>>>(static_cast<const float*>(w), T, B, bits);
+  else
+    whit::pack_mask<double><<<grid, 256, 0, s>>>(static_cast<const double*>(w), T, B, bits);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "pack launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
 }
 
@@ -550,6 +614,10 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
   if (ws->irr) {
     if ((st = encode_map(&p.tm_lw, ws->times, ws->dt, ws->B, ws->T, kK + 2 * ws->d)) != WHIT_OK) return st;
     return dispatch_irr<true>(ws, p);
+  }
+  if (ws->wbits) {
+    p.wbits = ws->wbits;
+    return dispatch_wb<true>(ws, p);
   }
   return dispatch<true>(ws, p);
 }

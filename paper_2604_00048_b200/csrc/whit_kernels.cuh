@@ -61,6 +61,7 @@ struct Params {
   CUtensorMap tm_lw;      // LOSS: loss weights [T][B], box {32, K}
   CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
   void* loss;             // LOSS: per-series loss [B]
+  const uint32_t* wbits;  // WB: bit-packed 0/1 weights [ceil(T/32)][B], bit t%32 of word t/32
   double* ck_fac;         // factor checkpoints [C][NFAC][B] (written by band 0, read by all bands)
   double* ck_rhs_f;       // forward rhs checkpoints [C][nb][d][B]
   double* ck_rhs_b;       // backward rhs checkpoints [C][nb][d][B]
@@ -277,12 +278,12 @@ template <typename IO, int D, bool BWD> struct Tile {
 };
 constexpr int kMaxBands = 10;
 
-template <int D, typename IO, bool PD, bool BWD, bool LOSS = false> struct Layout {
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false> struct Layout {
   static constexpr int K = Tile<IO, D, BWD>::K, ST = Tile<IO, D, BWD>::ST, WARPS = Tile<IO, D, BWD>::WARPS;
   static constexpr int ROW = 32 * (int)sizeof(IO);  // bytes of one staged time row (one warp)
   static constexpr int OFF_RHS = 0;
-  static constexpr int OFF_W = K * ROW;
-  static constexpr int OFF_LAM = 2 * K * ROW;
+  static constexpr int OFF_W = K * ROW;                        // (absent with WB: w comes as bits)
+  static constexpr int OFF_LAM = (WB ? 1 : 2) * K * ROW;
   static constexpr int OFF_DZ = OFF_LAM + (PD ? (K + D) * ROW : 0);
   static constexpr int OFF_LW = OFF_DZ + (BWD ? K * ROW : 0);  // LOSS (forward): loss-weight tile
   static constexpr int STAGE = (OFF_LW + (LOSS ? K * ROW : 0) + 127) / 128 * 128;
@@ -293,21 +294,21 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false> struct Layou
   static constexpr int SMEM = WARPS * WARP_SMEM;
   // multi-band CTA of nb warps: rings + reduction tile + scalar slots
   static constexpr int smem_mb(int nb) { return nb * WARP_SMEM + OUT + nb * 32 * 8; }
-  static constexpr uint32_t BYTES_UP = (2 * K + (PD ? K : 0)) * ROW;
-  static constexpr uint32_t BYTES_DN = (2 * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
+  static constexpr uint32_t BYTES_UP = ((WB ? 1 : 2) * K + (PD ? K : 0)) * ROW;
+  static constexpr uint32_t BYTES_DN = ((WB ? 1 : 2) * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
 };
 
 // Issue tile i (up sweep tiles 0..C-1, then down sweep C-1..0) of one warp.
-template <int D, typename IO, bool PD, bool BWD, bool LOSS = false>
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
 __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage, uint64_t* bar, int i, int C,
                                            int c0, int band) {
-  using L = Layout<D, IO, PD, BWD, LOSS>;
+  using L = Layout<D, IO, PD, BWD, LOSS, WB>;
   const bool up = i < C;
   const int c = up ? i : 2 * C - 1 - i;
   const int t0 = c * L::K;
   mbar_arrive_expect_tx(bar, up ? L::BYTES_UP : L::BYTES_DN);
   tma_load_3d(stage + L::OFF_RHS, &p.tm_rhs, c0, t0, band, bar);
-  tma_load_2d(stage + L::OFF_W, &p.tm_w, c0, t0, bar);
+  if (!WB) tma_load_2d(stage + L::OFF_W, &p.tm_w, c0, t0, bar);
   if (PD) {
     if (up) tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_up, c0, t0, bar);
     else tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_dn, c0, t0 - D, bar);
@@ -317,15 +318,28 @@ __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage
 }
 
 // ------------------------------------------------------------------ per-thread sweep bodies
-template <int D, typename IO, bool PD, bool BWD, bool LOSS = false>
+// Weight of row k of a chunk: from the staged w tile, or (WB) bit k of the chunk's mask.
+template <typename IO, bool WB>
+__device__ __forceinline__ void row_w(const IO* t_w, uint32_t wm, int k, IO& wio, double& w) {
+  if (WB) {
+    const bool on = (wm >> k) & 1u;
+    wio = on ? IO(1) : IO(0);
+    w = on ? 1.0 : 0.0;
+  } else {
+    wio = t_w[k * 32];
+    w = to_f64<IO>(wio);
+  }
+}
+
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
 struct Sweep {
-  using L = Layout<D, IO, PD, BWD, LOSS>;
+  using L = Layout<D, IO, PD, BWD, LOSS, WB>;
   static constexpr int K = L::K;
 
   // ---- up sweep over one chunk (rows t0..t0+K-1); RAGGED: the chunk reaches row T-D or beyond
   template <bool RAGGED>
   static __device__ __forceinline__ void up_chunk(FState<D>& st, const unsigned char* stg, int lane, int t0, int T,
-                                                  double lam_s, int& nobs, bool& pos) {
+                                                  double lam_s, int& nobs, bool& pos, uint32_t wm = 0) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;
@@ -334,15 +348,16 @@ struct Sweep {
     for (int k = 0; k < K; ++k) {
       const int t = t0 + k;
       if (RAGGED && t >= T) break;  // rows past the end: nothing uses the state after row T-1
-      const IO wio = t_w[k * 32];
-      const double w = to_f64<IO>(wio);
+      IO wio;
+      double w;
+      row_w<IO, WB>(t_w, wm, k, wio, w);
       double lt = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
       if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double A[D], Dt, idt, vt;
       ldl_step<D, Newton<IO>::N>(st, w, lt, bb, A, Dt, idt, vt);
       if (!BWD) {
-        nobs += (wio > IO(0));
+        if (!WB) nobs += (wio > IO(0));  // (WB: counted per chunk with popc)
         pos = pos && (Dt > 0.0);  // all pivots positive (false on NaN); exact index found in a cold path
       }
     }
@@ -353,7 +368,7 @@ struct Sweep {
   // from the checkpoint the up sweep stored for it, with exactly the state
   // restore of the down sweep and the same ldl_step (bitwise-identical).
   static __device__ __noinline__ int first_bad_row(const Params& p, int c, long long b, const unsigned char* stg,
-                                                   int lane, int t0, int T, double lam_s) {
+                                                   int lane, int t0, int T, double lam_s, uint32_t wm = 0) {
     constexpr int NFAC = Ck<D>::NFAC;
     const long long B = p.B;
     const double* ck = p.ck_fac + (long long)c * NFAC * B + b;
@@ -376,8 +391,9 @@ struct Sweep {
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;
     for (int k = 0; k < K && t0 + k < T; ++k) {
       const int t = t0 + k;
-      const IO wio = t_w[k * 32];
-      const double w = to_f64<IO>(wio);
+      IO wio;
+      double w;
+      row_w<IO, WB>(t_w, wm, k, wio, w);
       const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : (t < T - D ? lam_s : 0.0);
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double A[D], Dt, idt, vt;
@@ -396,7 +412,7 @@ struct Sweep {
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
-                                                    double two_over_T = 0.0) {
+                                                    double two_over_T = 0.0, uint32_t wm = 0) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -407,8 +423,9 @@ struct Sweep {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int t = t0 + k;
-      const IO wio = t_w[k * 32];
-      const double w = to_f64<IO>(wio);
+      IO wio;
+      double w;
+      row_w<IO, WB>(t_w, wm, k, wio, w);
       double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
       if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
@@ -452,10 +469,10 @@ struct Sweep {
       } else {
         if (sizeof(IO) == 4 && PD) {
           // fp32 I/O: w*u and -(Du)(Dz) formed from u, Du rounded once to fp32 (<= 1.5 ulp fp32)
-          so0[k * 32] = t_w[k * 32] * from_f64<IO>(z);
+          so0[k * 32] = WB ? (((wm >> k) & 1u) ? from_f64<IO>(z) : IO(0)) : t_w[k * 32] * from_f64<IO>(z);
           so1[k * 32] = -(from_f64<IO>(dz) * t_dz[k * 32]);  // D z tile is 0 past row T-d-1
         } else {
-          const double w = to_f64<IO>(t_w[k * 32]);
+          const double w = WB ? (((wm >> k) & 1u) ? 1.0 : 0.0) : to_f64<IO>(t_w[k * 32]);
           so0[k * 32] = from_f64<IO>(w * z);
           const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
           if (PD) so1[k * 32] = from_f64<IO>(g);
@@ -479,12 +496,13 @@ struct Sweep {
 //               the factor (band 0 writes its checkpoints, every band reads
 //               them) and, in the backward, reduce -(Du_c)(Dz_c) over bands in
 //               shared memory in band order (deterministic).
-template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false>
+template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false, bool WB = false>
 __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Tile<IO, D, BWD>::MAXREG))
     whit_kernel(const __grid_constant__ Params p) {
   static_assert(!LOSS || (!BWD && !MB), "the fused loss is a single-band forward variant");
-  using L = Layout<D, IO, PD, BWD, LOSS>;
-  using S = Sweep<D, IO, PD, BWD, LOSS>;
+  static_assert(!WB || (!MB && !LOSS), "bit-packed W is a single-band fwd/bwd variant");
+  using L = Layout<D, IO, PD, BWD, LOSS, WB>;
+  using S = Sweep<D, IO, PD, BWD, LOSS, WB>;
   constexpr int K = L::K, ST = L::ST;
   constexpr int NFAC = Ck<D>::NFAC;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -513,7 +531,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < ST && i < ntiles; ++i)
-      issue_tile<D, IO, PD, BWD, LOSS>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw, band);
   }
   __syncwarp();
 
@@ -527,10 +545,19 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
   int nobs = 0, bad = 0;
   bool allpos = true;
   int it = 0;
+  // WB: the chunk's mask bits, prefetched one chunk ahead (plain coalesced 4-B loads)
+  auto wword = [&](int cc) -> uint32_t {
+    if (!WB || !valid || cc < 0 || cc >= C) return 0u;
+    const uint32_t word = p.wbits[(long long)((cc * K) >> 5) * B + b];
+    return (word >> ((cc * K) & 31)) & (K >= 32 ? 0xffffffffu : ((1u << K) - 1u));
+  };
+  uint32_t wm_next = wword(0);
 
   // ================================================================ up sweep
   for (int c = 0; c < C; ++c, ++it) {
     const int s = it % ST;
+    const uint32_t wm = wm_next;
+    wm_next = wword(c + 1);
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const unsigned char* stg = ring + s * L::STAGE;
     const int t0 = c * K;
@@ -550,15 +577,16 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
       for (int i = 0; i < D; ++i) ck[(long long)i * B] = st.v[i];
     }
     bool pos = true;
-    if (c < cr) S::template up_chunk<false>(st, stg, lane, t0, T, lam_s, nobs, pos);
-    else S::template up_chunk<true>(st, stg, lane, t0, T, lam_s, nobs, pos);
+    if (c < cr) S::template up_chunk<false>(st, stg, lane, t0, T, lam_s, nobs, pos, wm);
+    else S::template up_chunk<true>(st, stg, lane, t0, T, lam_s, nobs, pos, wm);
+    if (WB && !BWD) nobs += __popc(wm);  // bits past T are 0 (packing)
     allpos = allpos && pos;
     // exact failing row (cold): band 0 only -- it wrote the factor checkpoint it replays from
-    if (!BWD && !pos && bad == 0 && valid && band == 0) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s);
+    if (!BWD && !pos && bad == 0 && valid && band == 0) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s, wm);
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD, LOSS>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }
   }
 
@@ -602,9 +630,12 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     }                                                                                             \
   } while (0)
   WHIT_LOAD_CK(C - 1);
+  wm_next = wword(C - 1);
 
   for (int c = C - 1; c >= 0; --c, ++it) {
     const int s = it % ST;
+    const uint32_t wm = wm_next;
+    wm_next = wword(c - 1);
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const unsigned char* stg = ring + s * L::STAGE;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -640,10 +671,10 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     const double two_over_T = 2.0 / (double)T;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    so2 + lane, two_over_T);
+                                    so2 + lane, two_over_T, wm);
     else
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   so2 + lane, two_over_T);
+                                   so2 + lane, two_over_T, wm);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
     if (lane == 0) {
@@ -675,7 +706,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     if (lane == 0 && it + ST < ntiles) {
       if (L::INPLACE) bulk_wait_read0();  // the stores read this very stage
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD, LOSS>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }
   }
 #undef WHIT_LOAD_CK
@@ -1272,6 +1303,22 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
     __syncwarp();
   }
   if (lane == 0) bulk_wait0();
+}
+
+// Bit-pack a 0/1 weight plane: word r of series b holds w[32r + j][b] != 0 in bit j (0 past T).
+template <typename IO>
+__global__ void pack_mask(const IO* __restrict__ w, long long T, long long B, uint32_t* __restrict__ bits) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long r = blockIdx.y;
+  if (b >= B) return;
+  uint32_t word = 0;
+  const long long t0 = r * 32;
+#pragma unroll 8
+  for (int j = 0; j < 32; ++j) {
+    const long long t = t0 + j;
+    if (t < T && w[t * B + b] != IO(0)) word |= 1u << j;
+  }
+  bits[r * B + b] = word;
 }
 
 // Count of failed series (info != 0) for whit_failures.

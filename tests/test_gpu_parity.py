@@ -461,3 +461,36 @@ def test_irregular_unit_spacing_equals_daily_path():
     ref = run_cuda(x, d, torch.float64, backward=False)
     torch.cuda.synchronize()
     assert np.max(np.abs(z.cpu().numpy().T - ref["z"])) <= 1e-12 * np.max(np.abs(ref["z"]))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_wbits_bitwise_equal_dense(d, per_date, dtype):
+    """Bit-packed W (the paper's binary W) gives results bitwise identical to the dense 0/1
+    float plane, forward and backward; the packing kernel sets bit j of word r iff w[32r+j] != 0."""
+    import paper_2604_00048_b200 as P
+
+    T, B = 203, 132
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", dtype=dtype, seed=60 + d)
+    ref = run_cuda(x, d, dtype)
+    bits = P.whit_pack_mask(x["w"])
+    wb = x["w"].cpu().numpy() != 0
+    bh = bits.cpu().numpy().view(np.uint32)
+    for r in (0, 3, bh.shape[0] - 1):
+        for j in (0, 5, 31):
+            t = 32 * r + j
+            exp = wb[t] if t < T else np.zeros(B, bool)
+            assert np.array_equal(((bh[r] >> j) & 1).astype(bool), exp)
+    ws = P.Workspace(d, T, B, dtype, per_date)
+    z, gy, gl = torch.empty_like(x["y"]), torch.empty_like(x["y"]), torch.empty_like(x["lam"])
+    P.whit_forward_wbits(x["y"], bits, x["lam"], d, T, B, z, ws)
+    P.whit_backward(x["g"], ws, z, gy, gl)
+    nfail, info = P.whit_failures(ws, with_info=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(z.double().cpu().numpy().T, ref["z"])
+    assert np.array_equal(gy.double().cpu().numpy().T, ref["ybar"])
+    g = gl.double().cpu().numpy()
+    assert np.array_equal(g.T if g.ndim == 2 else g, ref["lambar"])
+    assert np.array_equal(info, ref["info"])
