@@ -691,7 +691,9 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
       for (int k = warp; k < K; k += nb) {
         double acc = 0.0;
         for (int cb = 0; cb < nb; ++cb)
-          acc += to_f64<IO>(reinterpret_cast<const IO*>(smem + cb * L::WARP_SMEM + s * L::STAGE + L::OFF_DZ)[k * 32 + lane]);
+          acc += to_f64<IO>(reinterpret_cast<const IO*>(smem + cb * L::WARP_SMEM +
+                                                        (L::INPLACE ? s * L::STAGE + L::OFF_DZ
+                                                                    : ST * L::STAGE + L::OUT))[k * 32 + lane]);
         red[k * 32 + lane] = from_f64<IO>(acc);
       }
       fence_proxy_async_smem();
