@@ -143,17 +143,19 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(B: int, T: int, d: int, esz: int, per_date: bool, K: int = 16):
+def algorithmic_bytes(B: int, T: int, d: int, esz: int, per_date: bool, K: int = 16, wbits: bool = False):
     """Bytes each launch must move in the R-mode design: inputs read in the
-    up sweep and re-read in the down sweep, outputs written once, fp64 checkpoints."""
+    up sweep and re-read in the down sweep, outputs written once, fp64 checkpoints.
+    wbits: W read as 1 bit per date (4-B words, one per 32 dates) instead of an esz plane."""
     C = math.ceil(T / K)
     nfac, nrhs = d + d * (d - 1) // 2, d
     lam_rows = (T - d) if per_date else 0
-    fwd = (2 * (2 * T + lam_rows) * esz            # y, w (+ lambda) read twice
+    wrow = (4 * math.ceil(T / 32) / T) if wbits else esz  # bytes of w per date
+    fwd = (2 * ((T + lam_rows) * esz + T * wrow)    # y, w (+ lambda) read twice
            + (T + (T - d)) * esz                    # z, D z written
            + 2 * C * (nfac + nrhs) * 8              # checkpoints written + read
            + (0 if per_date else esz)) * B          # scalar lambda
-    bwd = (2 * (2 * T + lam_rows) * esz            # g, w (+ lambda) read twice
+    bwd = (2 * ((T + lam_rows) * esz + T * wrow)    # g, w (+ lambda) read twice
            + (T - d) * esz                          # D z read
            + T * esz + (lam_rows * esz if per_date else esz)  # grad_y, grad_lambda written
            + C * nrhs * 8 * 2                       # rhs checkpoints written + read
@@ -363,6 +365,38 @@ def run_libwhit(args):
             "step_GBps_algorithmic": round((fb + bb) / (ms_step / 1e3) / 1e9, 1),
             "step_frac_of_min_bytes": round((mf + mb) / (ms_step / 1e3) / 1e9 / peak, 4)}
 
+    # the same step with the binary W bit-packed (whit_forward_wbits), reported beside the headline
+    wbits_line = None
+    if args.config == "hetero":
+        bits = P.whit_pack_mask(w)
+        for _ in range(3):
+            P.whit_forward_wbits(y, bits, lam, d, T, B, z, wsp)
+            P.whit_backward(g, wsp, z, gy, gl)
+        torch.cuda.synchronize(dev)
+        evb = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+        t_start.record(stream)
+        for i in range(K):
+            evb[i][0].record(stream)
+            P.whit_forward_wbits(y, bits, lam, d, T, B, z, wsp)
+            evb[i][1].record(stream)
+            P.whit_backward(g, wsp, z, gy, gl)
+            evb[i][2].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        msb = max_over_ranks(t_start.elapsed_time(t_end) / K, dev)
+        fbb, bbb, _, _ = algorithmic_bytes(B, T, d, esz, per_date, wbits=True)
+        fa = statistics.mean(e[0].elapsed_time(e[1]) for e in evb)
+        ba = statistics.mean(e[1].elapsed_time(e[2]) for e in evb)
+        domb, dms, dbytes = ("whit_backward", ba, bbb) if ba >= fa else ("whit_forward_wbits", fa, fbb)
+        ach = dbytes / (dms / 1e3) / 1e9
+        wbits_line = {"value": ws_n * B / (msb / 1e3), "unit": UNIT, "ms_per_step": msb,
+                      "w_format": "uint32 bit planes [ceil(T/32)][B] (binary W, P:26), whit_forward_wbits",
+                      "gpu_launches": 2 * K,
+                      "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                                   "frac": round(ach / peak, 4), "kernel": domb, "kernel_ms": round(dms, 4),
+                                   "algorithmic_bytes": dbytes, "fwd_ms": round(fa, 4), "bwd_ms": round(ba, 4)}}
+        del bits
+
     # end to end through the public API with host buffers (rank-local)
     e2e = None
     if not args.no_e2e:
@@ -394,6 +428,7 @@ def run_libwhit(args):
                        "mask": "Sentinel-2 revisit + seasonal clouds, 90-day trailing gap",
                        "failed_series": nfail},
             "roofline": roof, "gpu_launches": 2 * K, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+            "w_bits": wbits_line,
         }
         print(json.dumps(line), flush=True)
     if ws_n > 1:
