@@ -494,3 +494,74 @@ def test_wbits_bitwise_equal_dense(d, per_date, dtype):
     g = gl.double().cpu().numpy()
     assert np.array_equal(g.T if g.ndim == 2 else g, ref["lambar"])
     assert np.array_equal(info, ref["info"])
+
+
+@pytest.mark.parametrize("T", [3, 5, 9, 17])
+def test_edge_T_all_entry_points(T):
+    """Tiny T (below one chunk, = d+1) through bands, wbits, variance, fused loss and the irregular
+    grid: finite, and equal to the oracle."""
+    import paper_2604_00048_b200 as P
+
+    d, B = 2, 8
+    x = synth.make_inputs("toy", B=B, T=T, d=d, lam_mode="per_date", device="cuda", dtype=torch.float64, seed=T)
+    h = host_inputs(x)
+    # wbits
+    ws = P.Workspace(d, T, B, torch.float64, True)
+    z = torch.empty_like(x["y"])
+    P.whit_forward_wbits(x["y"], P.whit_pack_mask(x["w"]), x["lam"], d, T, B, z, ws)
+    # variance
+    var = torch.empty_like(x["y"])
+    P.whit_posterior_variance(x["w"], x["lam"], d, T, B, var, ws)
+    # irregular (unit-spaced)
+    tt = (torch.arange(T, dtype=torch.float64, device="cuda")[:, None] * 3.0).expand(T, B).contiguous()
+    wt = P.Workspace(d, T, B, torch.float64, True, times=True)
+    zt = torch.empty_like(x["y"])
+    P.whit_forward_times(x["y"], x["w"], x["lam"], tt, d, T, B, zt, wt)
+    # bands
+    xb = synth.make_inputs_bands("toy", 3, B=B, T=T, d=d, lam_mode="per_date", device="cuda", dtype=torch.float64, seed=T)
+    wsb = P.Workspace(d, T, B, torch.float64, True, C=3)
+    zb = torch.empty_like(xb["y"])
+    P.whit_forward_bands(xb["y"], xb["w"], xb["lam"], d, T, B, 3, zb, wsb)
+    torch.cuda.synchronize()
+    th = tt.cpu().numpy().T
+    for b in range(B):
+        o = O1.forward(h["y"][b], h["w"][b], h["lam"][b], d)[0].astype(float)
+        ym = max(ymax_observed(h["y"][b], h["w"][b]), 1e-300)
+        assert np.max(np.abs(z[:, b].cpu().numpy() - o)) / ym <= 1e-10
+        vr = O1.posterior_variance(h["w"][b], h["lam"][b], d).astype(float)
+        assert rel_series(var[:, b].cpu().numpy(), vr).max() <= 1e-10
+        ot = O1.forward_backward_times(h["y"][b], h["w"][b], h["lam"][b], th[b], d, np.zeros(T))["z"].astype(float)
+        assert np.max(np.abs(zt[:, b].cpu().numpy() - ot)) / ym <= 1e-10
+        Y = xb["y"][:, :, b].cpu().numpy()
+        ob = O1.forward_backward_bands(Y, xb["w"][:, b].cpu().numpy(), xb["lam"][:, b].cpu().numpy(), d, np.zeros_like(Y))
+        for c in range(3):
+            assert np.max(np.abs(zb[c, :, b].cpu().numpy() - ob["z"][c].astype(float))) <= 1e-10 * max(1.0, np.abs(Y).max())
+
+
+def test_lambda_stress_range():
+    """lambda up to the network's bound 1e10 and down to 1e-6: finite results; fp64 vs O1
+    reported with a looser bound outside the gated lambda <= 1e5 (BJ)."""
+    d, T, B = 2, 300, 64
+    for lo, hi, tol in ((-6, 0, 1e-10), (5, 10, 1e-6)):
+        x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64, seed=5)
+        gen = torch.Generator(device="cuda").manual_seed(lo + 100)
+        x["lam"] = 10 ** (lo + (hi - lo) * torch.rand(x["lam"].shape, device="cuda", generator=gen, dtype=torch.float64))
+        res = run_cuda(x, d, torch.float64)
+        h = host_inputs(x)
+        assert np.all(np.isfinite(res["z"])) and np.all(np.isfinite(res["ybar"]))
+        for b in range(0, B, 9):
+            o = O1.forward_backward(h["y"][b], h["w"][b], h["lam"][b], d, h["g"][b])
+            ez = np.max(np.abs(res["z"][b] - o["z"].astype(float))) / ymax_observed(h["y"][b], h["w"][b])
+            assert ez <= tol, (lo, hi, b, ez)
+
+
+def test_lambda_zero_w_one_identity_gpu():
+    """lambda = 0, w = 1: Omega = I, z = y to rounding (fp64), grad_y = g, grad_lambda = -(Dg)(Dy)."""
+    d, T, B = 2, 100, 32
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64)
+    x["w"] = torch.ones_like(x["w"])
+    x["lam"] = torch.zeros_like(x["lam"])
+    res = run_cuda(x, d, torch.float64)
+    h = host_inputs(x)
+    assert np.max(np.abs(res["z"] - h["y"])) <= 1e-14
+    assert np.max(np.abs(res["ybar"] - h["g"])) <= 1e-14
