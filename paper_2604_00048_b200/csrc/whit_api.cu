@@ -16,6 +16,7 @@
 #include <string>
 
 #include "whit_kernels.cuh"
+#include "whit_mb2.cuh"
 
 using whit::Params;
 
@@ -194,14 +195,47 @@ whit_status launch(const Params& p, cudaStream_t s) {
   return WHIT_OK;
 }
 
+// Multi-band with a shared factor warp (NEXT-1): CTA = nb band warps + 1 factor warp.
+template <int D, typename IO, bool PD, bool BWD>
+whit_status launch_mb2(const Params& p, cudaStream_t s) {
+  using L = whit::MB2Layout<D, IO, PD, BWD>;
+  constexpr int max_smem = L::smem(whit::kMaxBands);
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    attr_err = cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    max_smem < kSmemBudget ? max_smem : kSmemBudget);
+  });
+  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
+  const int smem = L::smem(p.nb);
+  if (smem > kSmemBudget) return fail(WHIT_ERR_SHAPE, "%d bands need %d B of shared memory", p.nb, smem);
+  const long long grid = (p.B + 31) / 32;
+  whit::whit_mb2_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(32 * (p.nb + 1)), smem, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return WHIT_OK;
+}
+
 template <typename IO, bool PD, bool BWD, bool MB>
 whit_status dispatch_d(int d, const Params& p, cudaStream_t s) {
+  if constexpr (MB) {
+    switch (d) {
+      case 1: return launch_mb2<1, IO, PD, BWD>(p, s);
+      case 2: return launch_mb2<2, IO, PD, BWD>(p, s);
+      case 3: return launch_mb2<3, IO, PD, BWD>(p, s);
+    }
+    return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+  } else {
   switch (d) {
     case 1: return launch<1, IO, PD, BWD, MB>(p, s);
     case 2: return launch<2, IO, PD, BWD, MB>(p, s);
     case 3: return launch<3, IO, PD, BWD, MB>(p, s);
   }
   return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+  }
 }
 
 template <typename IO, bool BWD, bool MB>
