@@ -565,3 +565,21 @@ def test_lambda_zero_w_one_identity_gpu():
     h = host_inputs(x)
     assert np.max(np.abs(res["z"] - h["y"])) <= 1e-14
     assert np.max(np.abs(res["ybar"] - h["g"])) <= 1e-14
+
+
+@pytest.mark.parametrize("C", [3, 10])
+def test_bands_bitwise_equal_independent_series(C):
+    """The shared-factor kernel runs each band through exactly the single-series fp64 sequence:
+    z and grad_y of every band equal the independent-series results (w, lambda replicated) bit for
+    bit; grad_lambda equals the band sum of the per-band gradients to fp32 rounding."""
+    d, T, B = 2, 203, 96
+    x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, device="cuda", seed=21)
+    res = run_cuda_bands(x, d, C, torch.float32)
+    ys = x["y"].permute(1, 0, 2).reshape(T, C * B).contiguous()
+    gs = x["g"].permute(1, 0, 2).reshape(T, C * B).contiguous()
+    ind = run_cuda({"y": ys, "w": x["w"].repeat(1, C), "lam": x["lam"].repeat(1, C), "g": gs}, d, torch.float32)
+    for c in range(C):
+        assert np.array_equal(res["z"][c], ind["z"][c * B:(c + 1) * B].T), c
+        assert np.array_equal(res["ybar"][c], ind["ybar"][c * B:(c + 1) * B].T), c
+    lsum = sum(ind["lambar"][c * B:(c + 1) * B] for c in range(C)).T
+    assert np.max(np.abs(res["lambar"] - lsum)) <= 1e-6 * np.max(np.abs(lsum))
