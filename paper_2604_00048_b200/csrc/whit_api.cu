@@ -642,9 +642,9 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
   if ((st = encode_map(&p.tm_out0, grad_y, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
   if (ws->lm == WHIT_LAMBDA_PER_DATE) {
     if ((st = encode_map(&p.tm_out1, grad_lambda, ws->dt, ws->B, ws->T - ws->d, kK)) != WHIT_OK) return st;
-  } else {
-    p.out1 = grad_lambda;
   }
+  p.out0 = grad_y;
+  p.out1 = grad_lambda;
   if (ws->irr) {
     if ((st = encode_map(&p.tm_lw, ws->times, ws->dt, ws->B, ws->T, kK + 2 * ws->d)) != WHIT_OK) return st;
     return dispatch_irr<true>(ws, p);

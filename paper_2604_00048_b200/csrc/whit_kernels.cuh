@@ -57,7 +57,8 @@ struct Params {
   CUtensorMap tm_out1;    // forward: D z cache [nb][T-d][B] (3-D); backward: per-date grad_lambda [T-d][B] (2-D)
   const void* lam_scalar; // [B] (scalar lambda mode)
   const void* lam_plane;  // [T-d][B] (per-date mode; read directly only by the cold failure path)
-  void* out1;             // backward, scalar lambda: grad_lambda [B]
+  void* out0;             // backward: grad_y [T][B] (direct stores)
+  void* out1;             // backward: grad_lambda, [T-d][B] per date (direct stores) or [B] scalar
   CUtensorMap tm_lw;      // LOSS: loss weights [T][B], box {32, K}
   CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
   void* loss;             // LOSS: per-series loss [B]
@@ -298,7 +299,10 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
   // backward: grad_y staged in the stage's g slot, grad_lambda in its D z slot (both consumed)
   static constexpr bool INPLACE = false;  // in-place backward staging measured slower (both kernels DRAM-bound)
-  static constexpr int WARP_SMEM = ST * STAGE + (INPLACE ? 0 : (LOSS ? 3 : 2) * OUT);  // ring (+ out0, out1, out2)
+  // backward: grad_y and grad_lambda go straight to HBM with coalesced 128-B warp stores (no
+  // staging): 16.9 KB of smem per warp, so 12 warps/SM fit (latency hiding under the power cap)
+  static constexpr bool DIRECT = false;  // measured: no gain over TMA-staged stores at 8 warps (DRAM/power-bound), homo slower
+  static constexpr int WARP_SMEM = ST * STAGE + ((INPLACE || DIRECT) ? 0 : (LOSS ? 3 : 2) * OUT);
   static constexpr int SMEM = WARPS * WARP_SMEM;
   // multi-band CTA of nb warps: rings + reduction tile + scalar slots
   static constexpr int smem_mb(int nb) { return nb * WARP_SMEM + OUT + nb * 32 * 8; }
@@ -420,7 +424,8 @@ struct Sweep {
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
-                                                    double two_over_T = 0.0, uint32_t wm = 0) {
+                                                    double two_over_T = 0.0, uint32_t wm = 0, IO* gy0 = nullptr,
+                                                    IO* gl0 = nullptr, long long Bst = 0, bool valid = false) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -475,16 +480,24 @@ struct Sweep {
           if (!RAGGED || t < T) lam_acc = fma(lwe, e, lam_acc);  // (forward: lam_acc holds the loss sum)
         }
       } else {
+        IO gy, gl = IO(0);
         if (sizeof(IO) == 4 && PD) {
           // fp32 I/O: w*u and -(Du)(Dz) formed from u, Du rounded once to fp32 (<= 1.5 ulp fp32)
-          so0[k * 32] = WB ? (((wm >> k) & 1u) ? from_f64<IO>(z) : IO(0)) : t_w[k * 32] * from_f64<IO>(z);
-          so1[k * 32] = -(from_f64<IO>(dz) * t_dz[k * 32]);  // D z tile is 0 past row T-d-1
+          gy = WB ? (((wm >> k) & 1u) ? from_f64<IO>(z) : IO(0)) : t_w[k * 32] * from_f64<IO>(z);
+          gl = -(from_f64<IO>(dz) * t_dz[k * 32]);  // D z tile is 0 past row T-d-1
         } else {
           const double w = WB ? (((wm >> k) & 1u) ? 1.0 : 0.0) : to_f64<IO>(t_w[k * 32]);
-          so0[k * 32] = from_f64<IO>(w * z);
+          gy = from_f64<IO>(w * z);
           const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
-          if (PD) so1[k * 32] = from_f64<IO>(g);
+          if (PD) gl = from_f64<IO>(g);
           else if (!RAGGED || t < TmD) lam_acc += g;
+        }
+        if (L::DIRECT) {
+          if (valid && (!RAGGED || t < T)) gy0[(long long)k * Bst] = gy;
+          if (PD && valid && (!RAGGED || t < TmD)) gl0[(long long)k * Bst] = gl;
+        } else {
+          so0[k * 32] = gy;
+          if (PD) so1[k * 32] = gl;
         }
       }
     }
@@ -669,23 +682,25 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     if (c > 0) WHIT_LOAD_CK(c - 1);
 
     // the staging tiles must have been read by the previous chunk's TMA stores
-    if (!L::INPLACE) {
+    if (!L::INPLACE && !L::DIRECT) {
       if (lane == 0) bulk_wait_read0();
       __syncwarp();
-    } else {
+    } else if (L::INPLACE) {
       so0 = reinterpret_cast<IO*>(const_cast<unsigned char*>(stg) + L::OFF_RHS);
       so1 = reinterpret_cast<IO*>(const_cast<unsigned char*>(stg) + L::OFF_DZ);
     }
     const double two_over_T = 2.0 / (double)T;
+    IO* gy0 = L::DIRECT ? reinterpret_cast<IO*>(p.out0) + (long long)t0 * B + b : nullptr;
+    IO* gl0 = L::DIRECT && PD ? reinterpret_cast<IO*>(p.out1) + (long long)t0 * B + b : nullptr;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    so2 + lane, two_over_T, wm);
+                                    so2 + lane, two_over_T, wm, gy0, gl0, B, valid);
     else
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   so2 + lane, two_over_T, wm);
+                                   so2 + lane, two_over_T, wm, gy0, gl0, B, valid);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && !L::DIRECT) {
       tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
       if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
       if (LOSS) tma_store_3d(&p.tm_out2, so2, (int)bw, t0, 0);
