@@ -6,7 +6,11 @@ forward = ``whit_forward`` (Eq. (3), P:48), backward = ``whit_backward``
 stream only; all arithmetic runs in the library's kernels.
 
 Tensors are time-outer ``(T, B)`` (``lam``: ``(T-d, B)`` per date or ``(B,)``
-scalar per series), CUDA, contiguous, float32 or float64.
+scalar per series), CUDA, contiguous, float32 or float64.  Variants:
+
+* ``y`` of shape ``(C, T, B)``: C bands per pixel sharing ``w`` and ``lam``
+  (``whit_forward_bands``, NEXT-1); ``lam``'s gradient is summed over bands;
+* ``times=(T, B)``: uneven acquisition dates (``whit_forward_times``, NEXT-2).
 """
 from __future__ import annotations
 
@@ -17,19 +21,21 @@ from . import _lib as L
 
 def _pad_cols(x: torch.Tensor, Bp: int, value: float) -> torch.Tensor:
     if x.shape[-1] == Bp:
-        return x
+        return x.contiguous()
     pad = torch.full(x.shape[:-1] + (Bp - x.shape[-1],), value, dtype=x.dtype, device=x.device)
     return torch.cat([x, pad], dim=-1).contiguous()
 
 
 class WhittakerFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, y, w, lam, d):
+    def forward(ctx, y, w, lam, d, times=None):
         if not (y.is_cuda and w.is_cuda and lam.is_cuda):
             raise ValueError("libwhit runs on CUDA tensors only (no CPU fallback)")
-        if y.dim() != 2 or w.shape != y.shape:
-            raise ValueError("y and w must be (T, B)")
-        T, B = y.shape
+        bands = y.dim() == 3
+        C = y.shape[0] if bands else 1
+        T, B = y.shape[-2:]
+        if w.shape != (T, B):
+            raise ValueError(f"w must be (T, B) = {(T, B)}, got {tuple(w.shape)}")
         per_date = lam.dim() == 2
         if per_date and lam.shape != (T - d, B):
             raise ValueError(f"per-date lambda must be (T-d, B) = {(T - d, B)}, got {tuple(lam.shape)}")
@@ -37,32 +43,47 @@ class WhittakerFn(torch.autograd.Function):
             raise ValueError(f"scalar lambda must be (B,), got {tuple(lam.shape)}")
         if not (y.dtype == w.dtype == lam.dtype):
             raise TypeError("y, w, lambda must share a dtype")
+        if times is not None and (bands or times.shape != (T, B) or times.dtype != y.dtype):
+            raise ValueError("times must be (T, B) of y's dtype (single band)")
         q = 4 if y.dtype == torch.float32 else 2
         Bp = (B + q - 1) // q * q  # 16-byte row stride; padded series: w = 1, lam = 1, y = 0
-        yp = _pad_cols(y.contiguous(), Bp, 0.0)
-        wp = _pad_cols(w.contiguous(), Bp, 1.0)
-        lp = _pad_cols(lam.contiguous(), Bp, 1.0)
-        ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device)
+        yp = _pad_cols(y, Bp, 0.0)
+        wp = _pad_cols(w, Bp, 1.0)
+        lp = _pad_cols(lam, Bp, 1.0)
         z = torch.empty_like(yp)
-        L.whit_forward(yp, wp, lp, d, T, Bp, z, ws)
-        ctx.ws, ctx.keep, ctx.B, ctx.Bp, ctx.d = ws, (wp, lp, z), B, Bp, d
-        ctx.lam_shape = lam.shape
-        return z[:, :B] if Bp != B else z
+        if times is not None:
+            tp = times if Bp == B else torch.cat(
+                [times, torch.arange(T, dtype=times.dtype, device=times.device)[:, None].expand(T, Bp - B)], dim=1)
+            tp = tp.contiguous()
+            ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device, times=True)
+            L.whit_forward_times(yp, wp, lp, tp, d, T, Bp, z, ws)
+            keep = (wp, lp, z, tp)
+        elif bands:
+            ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device, C=C)
+            L.whit_forward_bands(yp, wp, lp, d, T, Bp, C, z, ws)
+            keep = (wp, lp, z)
+        else:
+            ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device)
+            L.whit_forward(yp, wp, lp, d, T, Bp, z, ws)
+            keep = (wp, lp, z)
+        ctx.ws, ctx.keep, ctx.B, ctx.Bp = ws, keep, B, Bp
+        return z[..., :B] if Bp != B else z
 
     @staticmethod
     def backward(ctx, gz):
-        ws, (wp, lp, z) = ctx.ws, ctx.keep
-        gzp = _pad_cols(gz.contiguous(), ctx.Bp, 0.0)
+        ws, keep = ctx.ws, ctx.keep
+        lp, z = keep[1], keep[2]
+        gzp = _pad_cols(gz, ctx.Bp, 0.0)
         gy = torch.empty_like(gzp)
         gl = torch.empty_like(lp)
         ws.set_stream()
         L.whit_backward(gzp, ws, z, gy, gl)
         B = ctx.B
         if ctx.Bp != B:
-            gy, gl = gy[:, :B], gl[..., :B]
-        return gy, None, gl, None
+            gy, gl = gy[..., :B], gl[..., :B]
+        return gy, None, gl, None, None
 
 
-def smooth(y: torch.Tensor, w: torch.Tensor, lam: torch.Tensor, d: int = 2) -> torch.Tensor:
-    """Differentiable Whittaker smoother (heteroscedastic if ``lam`` is (T-d, B))."""
-    return WhittakerFn.apply(y, w, lam, d)
+def smooth(y: torch.Tensor, w: torch.Tensor, lam: torch.Tensor, d: int = 2, times: torch.Tensor | None = None):
+    """Differentiable Whittaker smoother (heteroscedastic if ``lam`` is (T-d, B)); see module doc."""
+    return WhittakerFn.apply(y, w, lam, d, times)

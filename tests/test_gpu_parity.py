@@ -583,3 +583,33 @@ def test_bands_bitwise_equal_independent_series(C):
         assert np.array_equal(res["ybar"][c], ind["ybar"][c * B:(c + 1) * B].T), c
     lsum = sum(ind["lambar"][c * B:(c + 1) * B] for c in range(C)).T
     assert np.max(np.abs(res["lambar"] - lsum)) <= 1e-6 * np.max(np.abs(lsum))
+
+
+def test_autograd_bands_and_times():
+    """smooth() with (C, T, B) bands and with uneven times: gradients vs the oracles."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B, C = 2, 90, 10, 3
+    xb = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, device="cuda", dtype=torch.float64, seed=4)
+    y = xb["y"].clone().requires_grad_(True)
+    lam = xb["lam"].clone().requires_grad_(True)
+    z = P.smooth(y, xb["w"], lam, d)
+    gy, gl = torch.autograd.grad(z, (y, lam), grad_outputs=xb["g"])
+    for b in (0, 5, 9):
+        o = O1.forward_backward_bands(xb["y"][:, :, b].cpu().numpy(), xb["w"][:, b].cpu().numpy(),
+                                      xb["lam"][:, b].cpu().numpy(), d, xb["g"][:, :, b].cpu().numpy())
+        assert rel_series(z[:, :, b].detach().cpu().numpy().ravel(), o["z"].astype(float).ravel()).max() <= 1e-10
+        assert rel_series(gy[:, :, b].cpu().numpy().ravel(), o["ybar"].astype(float).ravel()).max() <= 1e-9
+        assert rel_series(gl[:, b].cpu().numpy(), o["lambar"]).max() <= 1e-9
+    x = synth.make_inputs("toy", B=B, T=T, d=d, lam_mode="per_date", device="cuda", dtype=torch.float64, seed=6)
+    tt = synth.make_times(B, T, device="cuda", dtype=torch.float64)
+    y1 = x["y"].clone().requires_grad_(True)
+    l1 = x["lam"].clone().requires_grad_(True)
+    z1 = P.smooth(y1, x["w"], l1, d, times=tt)
+    gy1, gl1 = torch.autograd.grad(z1, (y1, l1), grad_outputs=x["g"])
+    h = host_inputs(x)
+    th = tt.cpu().numpy().T
+    for b in (0, 7):
+        o = O1.forward_backward_times(h["y"][b], h["w"][b], h["lam"][b], th[b], d, h["g"][b])
+        assert rel_series(gy1[:, b].cpu().numpy(), o["ybar"]).max() <= 1e-9
+        assert rel_series(gl1[:, b].cpu().numpy(), o["lambar"]).max() <= 1e-9
