@@ -213,7 +213,8 @@ whit_status launch_mb2(const Params& p, cudaStream_t s) {
   const int smem = L::smem(p.nb);
   if (smem > kSmemBudget) return fail(WHIT_ERR_SHAPE, "%d bands need %d B of shared memory", p.nb, smem);
   const long long grid = (p.B + 31) / 32;
-  whit::whit_mb2_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(32 * (p.nb + 1)), smem, s>>>(p);
+  const int threads = 32 * (L::nwarps(p.nb) + 1);
+  whit::whit_mb2_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
@@ -496,6 +497,8 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   whit_status st = fill_params(ws, &p, y, w, lambda);
   if (st != WHIT_OK) return st;
   const int kK = ws->kk;
+  p.out0 = z;
+  p.out1 = ws->buf + ws->L.off_dz;
   if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
   if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
   ws->have_fwd = false;
@@ -645,6 +648,7 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
   }
   p.out0 = grad_y;
   p.out1 = grad_lambda;
+  p.dz_cache = ws->buf + ws->L.off_dz;
   if (ws->irr) {
     if ((st = encode_map(&p.tm_lw, ws->times, ws->dt, ws->B, ws->T, kK + 2 * ws->d)) != WHIT_OK) return st;
     return dispatch_irr<true>(ws, p);

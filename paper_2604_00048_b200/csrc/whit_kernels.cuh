@@ -57,7 +57,8 @@ struct Params {
   CUtensorMap tm_out1;    // forward: D z cache [nb][T-d][B] (3-D); backward: per-date grad_lambda [T-d][B] (2-D)
   const void* lam_scalar; // [B] (scalar lambda mode)
   const void* lam_plane;  // [T-d][B] (per-date mode; read directly only by the cold failure path)
-  void* out0;             // backward: grad_y [T][B] (direct stores)
+  void* out0;             // backward: grad_y [T][B] (direct stores); multi-band: z / grad_y [nb][T][B]
+  const void* dz_cache;   // multi-band backward: the forward's D z cache [nb][T-d][B]
   void* out1;             // backward: grad_lambda, [T-d][B] per date (direct stores) or [B] scalar
   CUtensorMap tm_lw;      // LOSS: loss weights [T][B], box {32, K}
   CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
