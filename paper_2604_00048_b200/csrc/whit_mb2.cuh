@@ -17,6 +17,7 @@
 // band's z and grad_y equal the independent-series results bit for bit; grad_lambda is the band
 // sum in fp64 (fixed order), reduced in shared memory.
 #pragma once
+#include <type_traits>
 #include "whit_kernels.cuh"
 
 namespace whit {
@@ -220,6 +221,7 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
   const int bj = warp;
   const int cb0 = bj * BPW;
   const bool two = cb0 + 1 < nb;
+  const bool ok1 = valid && two;  // this warp's second band exists
   unsigned char* ring = smem + L::OFF_BAND + bj * L::B_WARP;
   double* redw = reinterpret_cast<double*>(smem + L::OFF_BAND + nw * L::B_WARP);        // [nw][K][32] (PD bwd)
   double* redS = redw + (BWD && PD ? nw * K * 32 : 0);                                   // [nw][32]
@@ -266,25 +268,30 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
     const unsigned char* F = fbuf0 + (fb & 1) * L::FBUF;
     const double* FA = reinterpret_cast<const double*>(F + L::FB_A) + lane;
     const IO* FW = reinterpret_cast<const IO*>(F + L::FB_W) + lane;
-    const int n = min(K, T - t0);
+    auto up_rows = [&](auto tail_tag) {
+      constexpr bool TAIL = decltype(tail_tag)::value;  // the chunk reaches row T: stop there
+      const int n = T - t0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (k >= n) break;
-      const IO wio = FW[k * 32];
-      const double w = to_f64<IO>(wio);
+      for (int k = 0; k < K; ++k) {
+        if (TAIL && k >= n) break;
+        const IO wio = FW[k * 32];
+        const double w = to_f64<IO>(wio);
 #pragma unroll
-      for (int u = 0; u < BPW; ++u) {
-        double vv = rhs_times_w<IO, BWD>(t_rhs[(u * K + k) * 32], wio, w);
+        for (int u = 0; u < BPW; ++u) {
+          double vv = rhs_times_w<IO, BWD>(t_rhs[(u * K + k) * 32], wio, w);
 #pragma unroll
-        for (int j = D; j >= 1; --j) {
-          vv = fma(-Mj(D, j), v[u][j - 1], vv);
-          vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
+          for (int j = D; j >= 1; --j) {
+            vv = fma(-Mj(D, j), v[u][j - 1], vv);
+            vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
+          }
+#pragma unroll
+          for (int i = D - 1; i >= 1; --i) v[u][i] = v[u][i - 1];
+          v[u][0] = vv;
         }
-#pragma unroll
-        for (int i = D - 1; i >= 1; --i) v[u][i] = v[u][i - 1];
-        v[u][0] = vv;
       }
-    }
+    };
+    if (t0 + K > T) up_rows(std::true_type{});
+    else up_rows(std::false_type{});
     __syncwarp();
     if (lane == 0) mbar_arrive(&fac_empty[fb & 1]);
     if (lane == 0 && it + ST < ntiles) {
@@ -306,17 +313,26 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
   for (int c = C - 1; c >= 0; --c, ++it, ++fb) {
     const int s = it % ST;
     const int t0 = c * K;
+    // TAIL: the chunk holds rows >= T - D (the last d rows have no D z row; rows >= T none at all)
+    const bool tail = t0 + K > TmD;
     // backward: this chunk's D z rows of both bands, loaded now, used in the back substitution
     IO dzv[BPW][K];
     if (BWD) {
+      auto load_dz = [&](auto tail_tag) {
+        constexpr bool TAIL = decltype(tail_tag)::value;
 #pragma unroll
-      for (int u = 0; u < BPW; ++u)
+        for (int u = 0; u < BPW; ++u) {
+          const IO* src = dzc + ((long long)(cb0 + u) * TmD + t0) * B + b;
+          const bool ok = u == 0 ? valid : ok1;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int t = t0 + k;
-          dzv[u][k] = (valid && (u == 0 || two) && t < TmD)
-                          ? dzc[((long long)(cb0 + u) * TmD + t) * B + b] : IO(0);
+          for (int k = 0; k < K; ++k) {
+            dzv[u][k] = (ok && (!TAIL || t0 + k < TmD)) ? *src : IO(0);
+            src += B;
+          }
         }
+      };
+      if (tail) load_dz(std::true_type{});
+      else load_dz(std::false_type{});
     }
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const IO* t_rhs = reinterpret_cast<const IO*>(ring + s * L::B_STAGE) + lane;
@@ -354,49 +370,65 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
         q[u][k] = vv * idk;  // rows past T: FI = 0 -> q = 0
       }
     }
-#pragma unroll
-    for (int k = K - 1; k >= 0; --k) {
-      const int t = t0 + k;
-      const IO wio = FW[k * 32];
-      double a[D];
-#pragma unroll
-      for (int j = 1; j <= D; ++j) a[j - 1] = (k + j < K) ? FA[((k + j) * D + j - 1) * 32] : cA[k + j - K][j - 1];
-      double ls = 0.0;  // this warp's bands' -(D u)(D z) at row t (per-date backward)
+    auto back_rows = [&](auto tail_tag) {
+      constexpr bool TAIL = decltype(tail_tag)::value;
+      // output rows walked downwards from row t0 + K - 1
+      IO* o0[BPW];
+      IO* o1[BPW];
 #pragma unroll
       for (int u = 0; u < BPW; ++u) {
-        double z = q[u][k];
+        o0[u] = out0 + ((long long)(cb0 + u) * T + t0 + K - 1) * B + b;
+        o1[u] = out1 + ((long long)(cb0 + u) * TmD + t0 + K - 1) * B + b;
+      }
 #pragma unroll
-        for (int j = D; j >= 1; --j) {
-          z = fma(-Mj(D, j), zw[u][j - 1], z);
-          z = fma(-a[j - 1], zw[u][j - 1], z);
-        }
-        double dz = Cj(D, 0) * z;
+      for (int k = K - 1; k >= 0; --k) {
+        const int t = t0 + k;
+        const IO wio = FW[k * 32];
+        double a[D];
 #pragma unroll
-        for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[u][j - 1], dz);
+        for (int j = 1; j <= D; ++j) a[j - 1] = (k + j < K) ? FA[((k + j) * D + j - 1) * 32] : cA[k + j - K][j - 1];
+        double ls = 0.0;  // this warp's bands' -(D u)(D z) at row t (per-date backward)
 #pragma unroll
-        for (int i = D - 1; i >= 1; --i) zw[u][i] = zw[u][i - 1];
-        zw[u][0] = z;
-        const bool st_ok = valid && (u == 0 || two) && t < T;
-        const long long row = ((long long)(cb0 + u) * T + t) * B + b;
-        if (!BWD) {
-          if (st_ok) out0[row] = from_f64<IO>(z);
-          if (st_ok && t < TmD) out1[((long long)(cb0 + u) * TmD + t) * B + b] = from_f64<IO>(dz);
-        } else {
-          if (sizeof(IO) == 4 && PD) {
-            if (st_ok) out0[row] = wio * from_f64<IO>(z);
-            if (u == 0 || two) ls += to_f64<IO>(-(from_f64<IO>(dz) * dzv[u][k]));
+        for (int u = 0; u < BPW; ++u) {
+          double z = q[u][k];
+#pragma unroll
+          for (int j = D; j >= 1; --j) {
+            z = fma(-Mj(D, j), zw[u][j - 1], z);
+            z = fma(-a[j - 1], zw[u][j - 1], z);
+          }
+          double dz = Cj(D, 0) * z;
+#pragma unroll
+          for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[u][j - 1], dz);
+#pragma unroll
+          for (int i = D - 1; i >= 1; --i) zw[u][i] = zw[u][i - 1];
+          zw[u][0] = z;
+          const bool ok = u == 0 ? valid : ok1;
+          const bool in_t = !TAIL || t < T;
+          const bool in_dz = !TAIL || t < TmD;
+          if (!BWD) {
+            if (ok && in_t) *o0[u] = from_f64<IO>(z);
+            if (ok && in_dz) *o1[u] = from_f64<IO>(dz);
           } else {
-            if (st_ok) out0[row] = from_f64<IO>(to_f64<IO>(wio) * z);
-            const double g = -dz * to_f64<IO>(dzv[u][k]);
-            if (u == 0 || two) {
-              if (PD) ls += g;
-              else if (t < TmD) lam_acc += g;
+            if (sizeof(IO) == 4 && PD) {
+              if (ok && in_t) *o0[u] = wio * from_f64<IO>(z);
+              if (u == 0 || two) ls += to_f64<IO>(-(from_f64<IO>(dz) * dzv[u][k]));
+            } else {
+              if (ok && in_t) *o0[u] = from_f64<IO>(to_f64<IO>(wio) * z);
+              const double g = -dz * to_f64<IO>(dzv[u][k]);
+              if (u == 0 || two) {
+                if (PD) ls += g;
+                else if (in_dz) lam_acc += g;
+              }
             }
           }
+          o0[u] -= B;
+          o1[u] -= B;
         }
+        if (BWD && PD) redw[(bj * K + k) * 32 + lane] = ls;
       }
-      if (BWD && PD) redw[(bj * K + k) * 32 + lane] = ls;
-    }
+    };
+    if (tail) back_rows(std::true_type{});
+    else back_rows(std::false_type{});
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
