@@ -16,7 +16,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwhit.so")
+LIB_PATH = os.environ.get("WHIT_LIB_PATH") or os.path.join(_HERE, "libwhit.so")  # override: dev A/B builds
 
 WHIT_F32, WHIT_F64 = 0, 1
 WHIT_LAMBDA_SCALAR, WHIT_LAMBDA_PER_DATE = 0, 1

@@ -43,6 +43,12 @@ namespace {
 
 // chunk length = TMA tile rows (whit::Tile<IO, d>::K)
 int chunk_k(int d) { return d <= 2 ? 16 : 8; }
+// rows per chunk of the shared-factor multi-band kernel (MB2Layout::K)
+int chunk_k_bands(int d, int nb) {
+  if (nb <= 1) return chunk_k(d);
+  return d == 1 ? whit::MB2Layout<1, float, true, false>::K
+                : d == 2 ? whit::MB2Layout<2, float, true, false>::K : whit::MB2Layout<3, float, true, false>::K;
+}
 static_assert(whit::Tile<float, 1, false>::K == 16 && whit::Tile<float, 2, true>::K == 16 && whit::Tile<float, 3, false>::K == 8 &&
                   whit::Tile<double, 1, true>::K == 16 && whit::Tile<double, 2, false>::K == 16 && whit::Tile<double, 3, true>::K == 8,
               "chunk length table out of sync with whit::Tile");
@@ -61,7 +67,7 @@ bool layout(int d, int64_t T, int64_t B, int nb, whit_dtype dt, WsLayout* L, int
       (dt != WHIT_F32 && dt != WHIT_F64))
     return false;
   const size_t esz = dt == WHIT_F32 ? 4 : 8;
-  if (kk == 0) kk = chunk_k(d);
+  if (kk == 0) kk = chunk_k_bands(d, nb);
   const int64_t C = (T + kk - 1) / kk;
   const int nfac = d + d * (d - 1) / 2;
   size_t o = 0;
@@ -454,7 +460,7 @@ static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, 
   whit_ws* ws = new (std::nothrow) whit_ws;
   if (!ws) return fail(WHIT_ERR_ARG, "host allocation failed");
   ws->d = d; ws->T = T; ws->B = B; ws->nb = C; ws->dt = dtype; ws->lm = lambda_mode;
-  ws->irr = irr; ws->kk = irr ? 8 : chunk_k(d); ws->times = nullptr; ws->wbits = nullptr;
+  ws->irr = irr; ws->kk = irr ? 8 : chunk_k_bands(d, C); ws->times = nullptr; ws->wbits = nullptr;
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;

@@ -4,14 +4,14 @@
 // CTA = ceil(C/2) band warps (two bands each) + 1 factor warp over 32 pixels:
 //  * the factor warp streams w and lambda (its own TMA ring), runs the deviation-form LDL^T
 //    (ldl_step, R-10) once per pixel and publishes, per K-row chunk, the rows
-//    (A_{t,1..d}, 1/D_t, w_t) into one of two shared-memory factor buffers (mbarriers
+//    (A_{t,1..d}, 1/D_t, w_t) into a ring of NFB (3-4) shared-memory factor buffers (mbarriers
 //    fac_full / fac_empty); it writes the factor checkpoints and, in the down sweep, recomputes
 //    each chunk's factor from them;
 //  * each band warp streams its two bands' right-hand sides (TMA) and runs the 4-flop
 //    forward-substitution recurrences and the back substitutions with the published rows (two
 //    independent chains per lane = ILP), storing z / D z / grad_y straight to HBM with coalesced
 //    128-B warp stores (no staging), reading D z in the backward with plain loads issued a chunk
-//    ahead of use.  Shared memory per CTA (~77-80 KB at C = 10, fp32) lets two CTAs -- two
+//    ahead of use.  Shared memory per CTA (~105-113 KB at C = 10, fp32) lets two CTAs -- two
 //    independent pixel groups and factor chains -- share an SM.
 // The band warps execute exactly the fp64 operation sequence of the single-band kernel, so every
 // band's z and grad_y equal the independent-series results bit for bit; grad_lambda is the band
@@ -24,7 +24,10 @@ namespace whit {
 
 template <int D, typename IO, bool PD, bool BWD>
 struct MB2Layout {
-  static constexpr int K = D <= 2 ? 16 : 8, ST = 2, BPW = 2;  // bands per band warp
+#ifndef WHIT_MB2_K
+#define WHIT_MB2_K 8
+#endif
+  static constexpr int K = WHIT_MB2_K, ST = 2, BPW = 2;  // rows per chunk; bands per band warp
   static constexpr int ROW = 32 * (int)sizeof(IO);
   // factor warp ring: w K rows + lambda K+d rows
   static constexpr int F_OFF_W = 0, F_OFF_LAM = K * ROW;
@@ -39,21 +42,27 @@ struct MB2Layout {
   static constexpr uint32_t F_BYTES_DN = (K + (PD ? K + D : 0)) * ROW;
   // smem: factor ring | factor buffers x2 | band warps | per-warp reduction rows (fp64) + scalars
   static constexpr int OFF_FB = ST * F_STAGE;
-  static constexpr int OFF_BAND = OFF_FB + 2 * FBUF;
+  // factor buffers in flight: enough that the factor warp runs ahead of the band warps' jitter
+  static constexpr int NFB = (BWD && PD) ? 3 : 4;
+  static constexpr int OFF_BAND = OFF_FB + NFB * FBUF;
   __host__ __device__ static constexpr int nwarps(int nb) { return (nb + BPW - 1) / BPW; }
   static constexpr int smem(int nb) {
-    return OFF_BAND + nwarps(nb) * B_WARP + (BWD && PD ? nwarps(nb) * K * 32 * 8 : 0) + nwarps(nb) * 32 * 8;
+    return OFF_BAND + nwarps(nb) * B_WARP + (BWD && PD ? 2 * nwarps(nb) * K * 32 * 8 : 0) +
+           (BWD && !PD ? nwarps(nb) * 32 * 8 : 0);
   }
 };
 
+#ifndef WHIT_MB2_MAXREG
+#define WHIT_MB2_MAXREG 168
+#endif
 template <int D, typename IO, bool PD, bool BWD>
-__global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params p) {
+__global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_constant__ Params p) {
   using L = MB2Layout<D, IO, PD, BWD>;
   constexpr int K = L::K, ST = L::ST, NFAC = Ck<D>::NFAC, NW = Newton<IO>::N, BPW = L::BPW;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t f_full[ST];
   __shared__ __align__(8) uint64_t b_full[(kMaxBands + 1) / 2][ST];
-  __shared__ __align__(8) uint64_t fac_full[2], fac_empty[2];
+  __shared__ __align__(8) uint64_t fac_full[L::NFB], fac_empty[L::NFB];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nb = p.nb, nw = L::nwarps(nb), T = p.T, C = p.C, TmD = T - D;
@@ -67,7 +76,7 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
   unsigned char* fbuf0 = smem + L::OFF_FB;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < L::NFB; ++i) {
       mbar_init(&fac_full[i], 1);
       mbar_init(&fac_empty[i], nw);
     }
@@ -124,8 +133,8 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
 #pragma unroll
           for (int k = 0; k < D - 1 - m; ++k) ck[(long long)(f++) * B] = st.ap[m][k];
       }
-      mbar_wait(&fac_empty[fb & 1], (uint32_t)(((fb >> 1) & 1) ^ 1));
-      unsigned char* F = fbuf0 + (fb & 1) * L::FBUF;
+      mbar_wait(&fac_empty[fb % L::NFB], (uint32_t)(((fb / L::NFB) & 1) ^ 1));
+      unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
       double* FA = reinterpret_cast<double*>(F + L::FB_A) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
 #pragma unroll
@@ -146,7 +155,7 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&fac_full[fb & 1]);  // release: this warp's smem writes
+      if (lane == 0) mbar_arrive(&fac_full[fb % L::NFB]);  // release: this warp's smem writes
       if (lane == 0 && it + ST < ntiles) {
         fence_proxy_async_smem();
         issue(it + ST);
@@ -160,24 +169,32 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
       failed = valid ? (p.info[b] != 0) : true;
     }
     const double poison = failed ? qnan() : 0.0;
-    // ---- down sweep: recompute and publish each chunk's factor rows
+    // ---- down sweep: recompute and publish each chunk's factor rows.  The factor checkpoint of
+    // the next chunk is loaded one chunk ahead (its latency leaves the recurrence's chain).
+    double ckn[NFAC];
+    auto load_ck = [&](int c) {
+      const double* ckf = p.ck_fac + (long long)c * NFAC * B + b;
+#pragma unroll
+      for (int f = 0; f < NFAC; ++f) ckn[f] = valid ? ckf[(long long)f * B] : 0.0;
+    };
+    load_ck(C - 1);
     for (int c = C - 1; c >= 0; --c, ++it, ++fb) {
       const int s = it % ST;
+      {
+        int f = 0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) st.dl[i] = ckn[f++];
+#pragma unroll
+        for (int m = 0; m < D - 1; ++m)
+#pragma unroll
+          for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = ckn[f++];
+      }
+      if (c > 0) load_ck(c - 1);
       mbar_wait(&f_full[s], (uint32_t)((it / ST) & 1));
       const unsigned char* stg = ring + s * L::F_STAGE;
       const IO* t_w = reinterpret_cast<const IO*>(stg + L::F_OFF_W) + lane;
       const IO* t_lam = reinterpret_cast<const IO*>(stg + L::F_OFF_LAM) + lane;  // row k <-> t0 - D + k
       const int t0 = c * K;
-      if (valid) {
-        const double* ckf = p.ck_fac + (long long)c * NFAC * B + b;
-        int f = 0;
-#pragma unroll
-        for (int i = 0; i < D; ++i) st.dl[i] = ckf[(long long)(f++) * B];
-#pragma unroll
-        for (int m = 0; m < D - 1; ++m)
-#pragma unroll
-          for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = ckf[(long long)(f++) * B];
-      }
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         const int tj = t0 - 1 - i;
@@ -186,8 +203,8 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
         st.lm[i] = l;
         st.id[i] = (tj < 0) ? 1.0 : rcp64<NW>(l + st.dl[i]);
       }
-      mbar_wait(&fac_empty[fb & 1], (uint32_t)(((fb >> 1) & 1) ^ 1));
-      unsigned char* F = fbuf0 + (fb & 1) * L::FBUF;
+      mbar_wait(&fac_empty[fb % L::NFB], (uint32_t)(((fb / L::NFB) & 1) ^ 1));
+      unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
       double* FA = reinterpret_cast<double*>(F + L::FB_A) + lane;
       double* FI = reinterpret_cast<double*>(F + L::FB_ID) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
@@ -207,7 +224,7 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
         FW[k * 32] = wio;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&fac_full[fb & 1]);
+      if (lane == 0) mbar_arrive(&fac_full[fb % L::NFB]);
       if (lane == 0 && it + ST < ntiles) {
         fence_proxy_async_smem();
         issue(it + ST);
@@ -223,8 +240,8 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
   const bool two = cb0 + 1 < nb;
   const bool ok1 = valid && two;  // this warp's second band exists
   unsigned char* ring = smem + L::OFF_BAND + bj * L::B_WARP;
-  double* redw = reinterpret_cast<double*>(smem + L::OFF_BAND + nw * L::B_WARP);        // [nw][K][32] (PD bwd)
-  double* redS = redw + (BWD && PD ? nw * K * 32 : 0);                                   // [nw][32]
+  double* redw0 = reinterpret_cast<double*>(smem + L::OFF_BAND + nw * L::B_WARP);  // [2][nw][K][32] (PD bwd)
+  double* redS = redw0 + (BWD && PD ? 2 * nw * K * 32 : 0);                          // [nw][32]
   uint64_t* bars = b_full[bj];
   auto issue = [&](int i) {
     const bool up = i < C;
@@ -264,8 +281,8 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
         for (int i = 0; i < D; ++i) ck[(long long)i * B] = v[u][i];
       }
     }
-    mbar_wait(&fac_full[fb & 1], (uint32_t)((fb >> 1) & 1));
-    const unsigned char* F = fbuf0 + (fb & 1) * L::FBUF;
+    mbar_wait(&fac_full[fb % L::NFB], (uint32_t)((fb / L::NFB) & 1));
+    const unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
     const double* FA = reinterpret_cast<const double*>(F + L::FB_A) + lane;
     const IO* FW = reinterpret_cast<const IO*>(F + L::FB_W) + lane;
     auto up_rows = [&](auto tail_tag) {
@@ -293,7 +310,7 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
     if (t0 + K > T) up_rows(std::true_type{});
     else up_rows(std::false_type{});
     __syncwarp();
-    if (lane == 0) mbar_arrive(&fac_empty[fb & 1]);
+    if (lane == 0) mbar_arrive(&fac_empty[fb % L::NFB]);
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
       issue(it + ST);
@@ -310,43 +327,62 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
 #pragma unroll
     for (int i = 0; i < D; ++i) zw[u][i] = 0.0;
   double lam_acc = 0.0;
+  double vn[BPW][D];
+  auto load_v = [&](int c) {
+#pragma unroll
+    for (int u = 0; u < BPW; ++u) {
+      const double* ck = ck_rhs + (long long)c * ck_stride + (long long)(cb0 + u) * D * B;
+      const bool ok = u == 0 ? valid : ok1;
+#pragma unroll
+      for (int i = 0; i < D; ++i) vn[u][i] = ok ? ck[(long long)i * B] : 0.0;
+    }
+  };
+  load_v(C - 1);
+  // backward: D z rows of both bands, loaded one chunk ahead of the back substitution that uses them
+  IO dzn[BPW][K];
+  auto load_dz = [&](int c) {
+    const int t0 = c * K;
+    auto rows = [&](auto tail_tag) {
+      constexpr bool TAIL = decltype(tail_tag)::value;
+#pragma unroll
+      for (int u = 0; u < BPW; ++u) {
+        const IO* src = dzc + ((long long)(cb0 + u) * TmD + t0) * B + b;
+        const bool ok = u == 0 ? valid : ok1;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          dzn[u][k] = (ok && (!TAIL || t0 + k < TmD)) ? *src : IO(0);
+          src += B;
+        }
+      }
+    };
+    if (t0 + K > TmD) rows(std::true_type{});
+    else rows(std::false_type{});
+  };
+  if (BWD) load_dz(C - 1);
   for (int c = C - 1; c >= 0; --c, ++it, ++fb) {
     const int s = it % ST;
     const int t0 = c * K;
     // TAIL: the chunk holds rows >= T - D (the last d rows have no D z row; rows >= T none at all)
     const bool tail = t0 + K > TmD;
-    // backward: this chunk's D z rows of both bands, loaded now, used in the back substitution
     IO dzv[BPW][K];
+    double* const redw = redw0 + (c & 1) * nw * K * 32;
     if (BWD) {
-      auto load_dz = [&](auto tail_tag) {
-        constexpr bool TAIL = decltype(tail_tag)::value;
 #pragma unroll
-        for (int u = 0; u < BPW; ++u) {
-          const IO* src = dzc + ((long long)(cb0 + u) * TmD + t0) * B + b;
-          const bool ok = u == 0 ? valid : ok1;
+      for (int u = 0; u < BPW; ++u)
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            dzv[u][k] = (ok && (!TAIL || t0 + k < TmD)) ? *src : IO(0);
-            src += B;
-          }
-        }
-      };
-      if (tail) load_dz(std::true_type{});
-      else load_dz(std::false_type{});
+        for (int k = 0; k < K; ++k) dzv[u][k] = dzn[u][k];
+      if (c > 0) load_dz(c - 1);
     }
+    // this chunk's forward-substitution checkpoint (loaded one chunk ahead), then the next one's
+#pragma unroll
+    for (int u = 0; u < BPW; ++u)
+#pragma unroll
+      for (int i = 0; i < D; ++i) v[u][i] = vn[u][i];
+    if (c > 0) load_v(c - 1);
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const IO* t_rhs = reinterpret_cast<const IO*>(ring + s * L::B_STAGE) + lane;
-    if (valid) {
-#pragma unroll
-      for (int u = 0; u < BPW; ++u) {
-        if (u == 1 && !two) break;
-        const double* ck = ck_rhs + (long long)c * ck_stride + (long long)(cb0 + u) * D * B;
-#pragma unroll
-        for (int i = 0; i < D; ++i) v[u][i] = ck[(long long)i * B];
-      }
-    }
-    mbar_wait(&fac_full[fb & 1], (uint32_t)((fb >> 1) & 1));
-    const unsigned char* F = fbuf0 + (fb & 1) * L::FBUF;
+    mbar_wait(&fac_full[fb % L::NFB], (uint32_t)((fb / L::NFB) & 1));
+    const unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
     const double* FA = reinterpret_cast<const double*>(F + L::FB_A) + lane;
     const double* FI = reinterpret_cast<const double*>(F + L::FB_ID) + lane;
     const IO* FW = reinterpret_cast<const IO*>(F + L::FB_W) + lane;
@@ -424,7 +460,7 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
           o0[u] -= B;
           o1[u] -= B;
         }
-        if (BWD && PD) redw[(bj * K + k) * 32 + lane] = ls;
+        if (BWD && PD) redw[(bj * K + k) * 32 + lane] = ls;  // slot c & 1
       }
     };
     if (tail) back_rows(std::true_type{});
@@ -434,9 +470,11 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
 #pragma unroll
       for (int j = 0; j < D; ++j) cA[i][j] = FA[(i * D + j) * 32];
     __syncwarp();
-    if (lane == 0) mbar_arrive(&fac_empty[fb & 1]);
+    if (lane == 0) mbar_arrive(&fac_empty[fb % L::NFB]);
     if (BWD && PD) {
       // grad_lambda_r = sum over band warps (fixed order) of their two bands' -(D u)(D z)
+      // one barrier per chunk: slot c & 1 is written again two chunks later, after every warp
+      // has passed the next chunk's barrier, i.e. finished reducing this one
       named_bar_sync(1, 32 * nw);
       for (int k = bj; k < K; k += nw) {
         const int t = t0 + k;
@@ -444,7 +482,6 @@ __global__ void __maxnreg__(168) whit_mb2_kernel(const __grid_constant__ Params 
         for (int j = 0; j < nw; ++j) acc += redw[(j * K + k) * 32 + lane];
         if (valid && t < TmD) out1[(long long)t * B + b] = from_f64<IO>(acc);
       }
-      named_bar_sync(1, 32 * nw);  // redw reused next chunk
     }
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {

@@ -26,6 +26,8 @@ for _ in range(5):
 ms = min(tf) + min(tb)
 print(f"bands C={C} pixels={B} T={T}: fwd {min(tf):.3f} bwd {min(tb):.3f} ms -> {B*C/ms*1e3/1e6:.2f} M band-series/s "
       f"({B/ms*1e3/1e6:.2f} M pixels/s)")
+if os.environ.get("QB_ONLY"):
+    sys.exit(0)
 # independent-series baseline on the same band-series (w, lambda replicated per band)
 del ws, z, gy, gl
 x.clear()
