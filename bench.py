@@ -76,6 +76,22 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def gather_checksums(tensors, world: int) -> dict:
+    """Exact per-rank checksums: int64 sum of each tensor's bit patterns (order-independent, so equal
+    results give equal sums on any device), all-gathered across ranks (NCCL on the GPU, gloo in the
+    CPU tests) outside the timed region."""
+    import torch
+    import torch.distributed as dist
+    sums = torch.stack([t.view(torch.int32 if t.element_size() == 4 else torch.int64).sum(dtype=torch.int64)
+                        for t in tensors])
+    allsums = [sums]
+    if world > 1:
+        allsums = [torch.empty_like(sums) for _ in range(world)]
+        dist.all_gather(allsums, sums)
+    return {"kind": "int64 sum of the output bit patterns (z, grad_y, grad_lambda) per rank",
+            "per_rank": [[int(v) for v in a.tolist()] for a in allsums]}
+
+
 def measured_peak_gbs():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -347,6 +363,11 @@ def run_libwhit(args):
     ms_step = max_over_ranks(total_ms / K, dev)
     value = ws_n * B / (ms_step / 1e3)
 
+    # per-rank checksums of the outputs (exact: int64 sums of the bit patterns, order-independent), gathered
+    # over NCCL outside the timed region.  Rank r owns global series [r*B, (r+1)*B) at every N, so rank r's
+    # checksum is the same at every world size (results are bitwise independent of placement).
+    checksums = gather_checksums((z, gy, gl), ws_n)
+
     # roofline of the dominant kernel
     fb, bb, mf, mb = algorithmic_bytes(B, T, d, esz, per_date)
     f_avg, b_avg = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
@@ -428,7 +449,7 @@ def run_libwhit(args):
                        "mask": "Sentinel-2 revisit + seasonal clouds, 90-day trailing gap",
                        "failed_series": nfail},
             "roofline": roof, "gpu_launches": 2 * K, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
-            "w_bits": wbits_line,
+            "w_bits": wbits_line, "checksums": checksums,
         }
         print(json.dumps(line), flush=True)
     if ws_n > 1:

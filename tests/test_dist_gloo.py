@@ -30,8 +30,9 @@ def _worker(rank, world, port, q):
     x = synth.make_inputs("hetero", B=B, T=80, series_offset=off)
     gathered = [None] * world
     dist.all_gather_object(gathered, (off, B, {k: x[k].clone() for k in ("y", "w", "lam", "g")}))
+    cks = bench.gather_checksums((x["y"], x["lam"]), world)
     if rank == 0:
-        q.put((mx, gathered))
+        q.put((mx, gathered, cks))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -43,7 +44,7 @@ def test_world2_shards_timing_and_rank_independent_inputs():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    mx, gathered = q.get(timeout=240)
+    mx, gathered, cks = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -54,6 +55,14 @@ def test_world2_shards_timing_and_rank_independent_inputs():
     full = synth.make_inputs("hetero", B=128, T=80)
     for k in ("y", "w", "lam", "g"):
         assert torch.equal(torch.cat([x0[k], x1[k]], dim=-1), full[k]), k
+    # gathered checksums: one row per rank, each the exact bit-pattern sum of that rank's shard
+    import bench
+    assert len(cks["per_rank"]) == 2
+    for r, xr in enumerate((x0, x1)):
+        assert cks["per_rank"][r] == bench.gather_checksums((xr["y"], xr["lam"]), 1)["per_rank"][0]
+    # order-independent: the sum over both shards equals the checksum of the full batch
+    tot = bench.gather_checksums((full["y"], full["lam"]), 1)["per_rank"][0]
+    assert [a + b for a, b in zip(*cks["per_rank"])] == tot
 
 
 def test_max_over_ranks_without_group_is_identity():
