@@ -613,3 +613,35 @@ def test_autograd_bands_and_times():
         o = O1.forward_backward_times(h["y"][b], h["w"][b], h["lam"][b], th[b], d, h["g"][b])
         assert rel_series(gy1[:, b].cpu().numpy(), o["ybar"]).max() <= 1e-9
         assert rel_series(gl1[:, b].cpu().numpy(), o["lambar"]).max() <= 1e-9
+
+
+def test_s2tile_full_shape_sampled():
+    """BASELINE configs[3] at the per-GPU shard bench.py times (10 bands x 131,072 pixels, T = 3,288,
+    per-date lambda, fp32, the launch configuration of `bench.py --config s2tile`): sampled pixels vs O1
+    (one dense factor per pixel, 10 right-hand sides), whole-batch finiteness and no failures."""
+    import paper_2604_00048_b200 as P
+
+    d, C = 2, 10
+    x = synth.make_inputs_bands("hetero", C, B=131072, device="cuda")
+    y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
+    _, T, B = y.shape
+    ws = P.Workspace(d, T, B, torch.float32, True, C=C)
+    z, gy, gl = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam)
+    P.whit_forward_bands(y, w, lam, d, T, B, C, z, ws)
+    P.whit_backward_bands(g, ws, z, gy, gl)
+    assert P.whit_failures(ws) == 0
+    for t in (z, gy, gl):
+        assert bool(torch.isfinite(t).all())
+    tz, tg = TOL[(torch.float32, d)]
+    for b in _sample(B, 3):
+        Y = y[:, :, b].double().cpu().numpy()
+        G = g[:, :, b].double().cpu().numpy()
+        wb = w[:, b].double().cpu().numpy()
+        lb = lam[:, b].double().cpu().numpy()
+        o = O1.forward_backward_bands(Y, wb, lb, d, G)
+        zb, yb = z[:, :, b].double().cpu().numpy(), gy[:, :, b].double().cpu().numpy()
+        for c in range(C):
+            ez = np.max(np.abs(zb[c] - o["z"][c].astype(float))) / ymax_observed(Y[c], wb)
+            assert ez <= tz, (b, c, ez)
+            assert rel_series(yb[c], o["ybar"][c]).max() <= tg, (b, c)
+        assert rel_series(gl[:, b].double().cpu().numpy(), o["lambar"]).max() <= tg, b
