@@ -290,11 +290,23 @@ template <int D> struct Ck {
 // place to reach 12 warps measured no faster (slower on small batches).
 // Multi-band (MB): one CTA = nb warps (one band each) over the same 32 pixels,
 // <= 168 regs so that up to 12 warps fit one CTA.
+#ifndef WHIT_TILE_K2
+#define WHIT_TILE_K2 16
+#endif
+#ifndef WHIT_FWD_MAXREG
+#define WHIT_FWD_MAXREG 168
+#endif
+#ifndef WHIT_BWD_MAXREG
+#define WHIT_BWD_MAXREG 200
+#endif
+#ifndef WHIT_BWD_WARPS
+#define WHIT_BWD_WARPS 2
+#endif
 template <typename IO, int D, bool BWD> struct Tile {
-  static constexpr int K = D <= 2 ? 16 : 8;
+  static constexpr int K = D <= 2 ? WHIT_TILE_K2 : 8;
   static constexpr int ST = 2;
-  static constexpr int WARPS = BWD ? 2 : 4;
-  static constexpr int MAXREG = BWD ? 200 : 168;  // SMSP register files (16K): 3 warps/SMSP need <= 168
+  static constexpr int WARPS = BWD ? WHIT_BWD_WARPS : 4;
+  static constexpr int MAXREG = BWD ? WHIT_BWD_MAXREG : WHIT_FWD_MAXREG;  // SMSP register files (16K): 3 warps/SMSP need <= 168
   static constexpr int MB_MAXREG = 168;  // registers are granted per 4 warps: 12 x 32 x 168 <= 64K
 };
 constexpr int kMaxBands = 10;
