@@ -246,6 +246,31 @@ def test_host_executor_matches_device_path_bitwise(dtype, per_date):
     assert np.array_equal(info.numpy(), dev["info"])
 
 
+@pytest.mark.parametrize("chunk,nbuf", [(4096, 2), (96, 5)])
+def test_host_executor_forward_only_and_chunking(chunk, nbuf):
+    """whit_run_host without grad_z (forward only; info still reported), with one chunk larger than B
+    and with many small chunks (B % chunk != 0, more slots than needed at the end): z and info equal
+    the device path's bit for bit, including the NaN-poisoned failed series."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 257, 1000
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", seed=78)
+    x["w"][:, 5] = 0.0  # a failing series (fewer than d observed days)
+    x["w"][:, 6] = 0.0
+    x["w"][100, 6] = 1.0
+    dev = run_cuda(x, d, torch.float32)
+    assert dev["info"][5] == T - d + 1 and dev["info"][6] == T - d + 1
+    h = {k: x[k].cpu().pin_memory() for k in ("y", "w", "lam")}
+    z = torch.empty_like(h["y"]).pin_memory()
+    info = torch.empty(B, dtype=torch.int32).pin_memory()
+    P.whit_run_host(h["y"], h["w"], h["lam"], None, d, z, info=info, chunk=chunk, nbuf=nbuf)
+    torch.cuda.synchronize()
+    zz = z.double().numpy().T
+    assert np.array_equal(np.isnan(zz), np.isnan(dev["z"]))
+    assert np.array_equal(np.nan_to_num(zz, nan=0.0), np.nan_to_num(dev["z"], nan=0.0))
+    assert np.array_equal(info.numpy(), dev["info"])
+
+
 def run_cuda_bands(x: dict, d: int, C: int, dtype):
     import paper_2604_00048_b200 as P
 
