@@ -34,6 +34,7 @@ from .whittaker import (  # noqa: F401
     forward,
     backward,
     forward_backward,
+    weight_grad,
     forward_backward_bands,
     posterior_variance,
     mse_loss_grad,

@@ -166,6 +166,19 @@ def _grads(u, w, lam, d, z):
     return ybar, lamb
 
 
+def weight_grad(y, w, z, u):
+    """``dL/dw_t`` for the layer ``z = Omega^{-1} W y`` (NEXT-3's optional output).
+
+    Differentiating Eq. (3) in ``w_t``: ``Omega dz = e_t (y_t - z_t) dw_t``, so with
+    ``u = Omega^{-1} g``: ``dL/dw_t = u_t (y_t - z_t)``.  Reading R-19: at unobserved days
+    (``w_t = 0``) ``y_t`` carries no value (R-4) and the gradient is defined as 0.
+    """
+    y = np.asarray(y, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    ys = np.where(w > 0, y, 0.0).astype(LD)
+    return np.where(w > 0, np.asarray(u).astype(LD) * (ys - np.asarray(z).astype(LD)), LD(0))
+
+
 def forward_backward(y, w, lam, d: int, g, steps: int = 2) -> dict:
     """Forward and backward of one series sharing one factorization of Omega."""
     Om = omega_dense(w, lam, d)

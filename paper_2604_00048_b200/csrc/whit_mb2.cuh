@@ -27,7 +27,11 @@ struct MB2Layout {
 #ifndef WHIT_MB2_K
 #define WHIT_MB2_K 8
 #endif
-  static constexpr int K = WHIT_MB2_K, ST = 2, BPW = 2;  // rows per chunk; bands per band warp
+#ifndef WHIT_MB2_ST
+#define WHIT_MB2_ST 2
+#endif
+  // rows per chunk; TMA ring slots (ST - 1 chunks of loads in flight per warp); bands per band warp
+  static constexpr int K = WHIT_MB2_K, ST = WHIT_MB2_ST, BPW = 2;
   static constexpr int ROW = 32 * (int)sizeof(IO);
   // factor warp ring: w K rows + lambda K+d rows
   static constexpr int F_OFF_W = 0, F_OFF_LAM = K * ROW;

@@ -399,6 +399,30 @@ def test_gradients_central_fd(d, per_date):
     assert rel(out["lambar"], fd_l) < 1e-6
 
 
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_weight_grad_central_fd(d):
+    """dL/dw_t = u_t (y_t - z_t) (NEXT-3 option; Eq. (3) differentiated in w_t) == central finite
+    differences of L = g.z in w_t at every observed day, for soft weights; 0 at unobserved days (R-19)."""
+    T = 28
+    y = rng.normal(size=T)
+    w = np.where(rng.random(T) < 0.6, rng.uniform(0.2, 1.0, T), 0.0)
+    w[:d + 1] = rng.uniform(0.2, 1.0, d + 1)
+    y[w == 0] = np.nan  # unobserved values never enter (R-4)
+    lam = 10 ** rng.uniform(0, 2, T - d)
+    g = rng.normal(size=T)
+    out = O1.forward_backward(y, w, lam, d, g)
+    wg = O1.weight_grad(y, w, out["z"], out["u"]).astype(float)
+    assert np.all(wg[w == 0] == 0)
+
+    def L(wv):
+        return float(np.dot(g, O1.forward(y, wv, lam, d)[0].astype(float)))
+
+    h = 1e-6
+    obs = np.flatnonzero(w > 0)
+    fd = np.array([(L(w + h * np.eye(T)[t]) - L(w - h * np.eye(T)[t])) / (2 * h) for t in obs])
+    assert rel(wg[obs], fd) < 1e-7
+
+
 def test_eq4_explicit_column_contracts_to_lambar():
     """Eq. (4) as printed, dz/dlam_t = -Omega^{-1} d_t d_t^T z, contracted with g == lambar_t."""
     T, d = 30, 2
