@@ -150,6 +150,20 @@ whit_status whit_forward(const void* y, const void* w, const void* lambda, int d
 whit_status whit_backward(const void* grad_z, whit_ws* factor_ws, const void* z, void* grad_y,
                           void* grad_lambda);
 
+/* Gradient with respect to the observation weights (the optional output of
+ * NEXT-3; the paper keeps W fixed).  Differentiating Eq. (3)
+ * in w_t gives Omega dz = e_t (y_t - z_t) dw_t, so with u = Omega^{-1} g:
+ *   grad_w[t][b] = sum_c u_{c,t} (y_{c,t} - z_{c,t}),   u = grad_y / w,
+ * summed over the bands of a multi-band workspace (C = 1 otherwise).  Reading
+ * R-19: grad_w = 0 where w_t = 0 (y_t carries no value there, R-4); NaN for a
+ * failed series.  Call after whit_backward (or whit_backward_bands, or the
+ * irregular-grid backward) on the same workspace: y is the forward's input, z
+ * the forward's output (checked against the workspace), grad_y the backward's
+ * output; grad_w has w's shape [T][B] and dtype.  The float weight plane of the
+ * last forward is used (WHIT_ERR_STATE after whit_forward_wbits).  One
+ * element-wise kernel launch on the workspace stream. */
+whit_status whit_grad_w(whit_ws* factor_ws, const void* y, const void* z, const void* grad_y, void* grad_w);
+
 /* ---------------------------------------------------------------------------
  * Multi-band pixels (NEXT-1; the paper's "batched multivariate vectors", P:28,
  * C = 10 bands per pixel in its benchmark).  The C bands of a pixel
@@ -158,12 +172,14 @@ whit_status whit_backward(const void* grad_z, whit_ws* factor_ws, const void* z,
  *   y, z, grad_z, grad_y   [C][T][B]       (band planes stacked)
  *   w                      [T][B]           (shared)
  *   lambda, grad_lambda    [T-d][B] or [B]  (shared; grad_lambda is summed over
- *                                             bands, in band order, in fp64:
+ *                                             bands, in a fixed order, in fp64:
  *                                             dL/dlambda_r = -sum_c (D u_c)_r (D z_c)_r)
  * 1 <= C <= 10 for F32 planes, <= 5 for F64 (one CTA's shared memory holds the
- * C band pipelines).  The factor is formed once per pixel per sweep (every band's
- * warp recomputes it from the same w, lambda; band 0 stores its checkpoints),
- * so w, lambda and factor-checkpoint bytes are amortised over C bands.  The
+ * C band pipelines).  The factor is formed once per pixel per sweep by one
+ * factor warp and handed to the band warps through shared memory (two bands per
+ * band warp), so w, lambda and factor-checkpoint bytes and the factor's fp64
+ * work are amortised over C bands; every band's z and grad_y equal the
+ * single-band results bit for bit.  The
  * single-band entry points above are the C = 1 case (whit_forward on a C > 1
  * workspace is WHIT_ERR_SHAPE; whit_backward works for any C). */
 size_t whit_ws_bytes_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype, whit_lambda_mode lambda_mode);

@@ -36,6 +36,7 @@ SIGNATURES = [
     ("whit_ws_destroy", None, [_VP]),
     ("whit_forward", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_backward", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    ("whit_grad_w", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("whit_failures", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int32)]),
     ("whit_info_device", _VP, [_VP]),
     ("whit_ws_bytes_bands", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -164,6 +165,11 @@ def whit_backward_bands(grad_z, ws: Workspace, z, grad_y, grad_lambda):
 
 def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):
     _check(_lib.whit_backward(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)), "whit_backward")
+
+
+def whit_grad_w(ws: Workspace, y, z, grad_y, grad_w):
+    """dL/dw = sum over bands of (grad_y / w) (y - z), 0 where w = 0 (after whit_backward)."""
+    _check(_lib.whit_grad_w(ws.handle, _ptr(y), _ptr(z), _ptr(grad_y), _ptr(grad_w)), "whit_grad_w")
 
 
 def whit_forward_times(y, w, lam, times, d: int, T: int, B: int, z, ws: Workspace):

@@ -11,6 +11,9 @@ scalar per series), CUDA, contiguous, float32 or float64.  Variants:
 * ``y`` of shape ``(C, T, B)``: C bands per pixel sharing ``w`` and ``lam``
   (``whit_forward_bands``, NEXT-1); ``lam``'s gradient is summed over bands;
 * ``times=(T, B)``: uneven acquisition dates (``whit_forward_times``, NEXT-2).
+
+``w`` gets a gradient when it requires one: ``dL/dw_t = sum_c u_t (y_t - z_t)`` (``whit_grad_w``; 0 at
+``w_t = 0``, reading R-19).
 """
 from __future__ import annotations
 
@@ -67,6 +70,7 @@ class WhittakerFn(torch.autograd.Function):
             L.whit_forward(yp, wp, lp, d, T, Bp, z, ws)
             keep = (wp, lp, z)
         ctx.ws, ctx.keep, ctx.B, ctx.Bp = ws, keep, B, Bp
+        ctx.yp = yp if ctx.needs_input_grad[1] else None  # dL/dw needs y (whit_grad_w)
         return z[..., :B] if Bp != B else z
 
     @staticmethod
@@ -78,10 +82,15 @@ class WhittakerFn(torch.autograd.Function):
         gl = torch.empty_like(lp)
         ws.set_stream()
         L.whit_backward(gzp, ws, z, gy, gl)
+        gw = None
+        if ctx.yp is not None:
+            gw = torch.empty_like(keep[0])
+            L.whit_grad_w(ws, ctx.yp, z, gy, gw)
         B = ctx.B
         if ctx.Bp != B:
             gy, gl = gy[..., :B], gl[..., :B]
-        return gy, None, gl, None, None
+            gw = gw[..., :B] if gw is not None else None
+        return gy, gw, gl, None, None
 
 
 def smooth(y: torch.Tensor, w: torch.Tensor, lam: torch.Tensor, d: int = 2, times: torch.Tensor | None = None):

@@ -670,6 +670,31 @@ whit_status whit_backward_bands(const void* grad_z, whit_ws* ws, const void* z, 
   return whit_backward(grad_z, ws, z, grad_y, grad_lambda);
 }
 
+whit_status whit_grad_w(whit_ws* ws, const void* y, const void* z, const void* grad_y, void* grad_w) {
+  if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
+  if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "whit_grad_w without a preceding forward on this workspace");
+  if (ws->wbits || !ws->w) return fail(WHIT_ERR_STATE, "whit_grad_w needs the float weight plane (not bit-packed W)");
+  if (!y || !z || !grad_y || !grad_w) return fail(WHIT_ERR_ARG, "NULL data pointer");
+  if (z != ws->z) return fail(WHIT_ERR_STATE, "z is not the output of the matching forward");
+  if (grad_w == y || grad_w == z || grad_w == grad_y || grad_w == ws->w)
+    return fail(WHIT_ERR_ARG, "grad_w aliases an input");
+  DeviceGuard guard(ws->device);
+  if (!guard.ok) return fail(WHIT_ERR_CUDA, "cudaSetDevice(%d) failed", ws->device);
+  const int32_t* info = reinterpret_cast<const int32_t*>(ws->buf + ws->L.off_info);
+  const dim3 grid((unsigned)((ws->B + 255) / 256), (unsigned)std::min<int64_t>(ws->T, 1024));
+  if (ws->dt == WHIT_F32)
+    whit::grad_w_kernel<float><<<grid, 256, 0, ws->stream>>>(
+        static_cast<const float*>(ws->w), static_cast<const float*>(y), static_cast<const float*>(z),
+        static_cast<const float*>(grad_y), info, static_cast<float*>(grad_w), ws->T, ws->B, ws->nb);
+  else
+    whit::grad_w_kernel<double><<<grid, 256, 0, ws->stream>>>(
+        static_cast<const double*>(ws->w), static_cast<const double*>(y), static_cast<const double*>(z),
+        static_cast<const double*>(grad_y), info, static_cast<double*>(grad_w), ws->T, ws->B, ws->nb);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return WHIT_OK;
+}
+
 whit_status whit_posterior_variance(const void* w, const void* lambda, int d, int64_t T, int64_t B, void* var,
                                     whit_ws* ws) {
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");

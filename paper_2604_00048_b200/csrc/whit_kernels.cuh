@@ -1370,6 +1370,33 @@ __global__ void pack_mask(const IO* __restrict__ w, long long T, long long B, ui
   bits[r * B + b] = word;
 }
 
+// dL/dw (NEXT-3 option): gw[t][b] = sum_c u_{c,t} (y_{c,t} - z_{c,t}) with u = grad_y / w (grad_y = W u,
+// Eq. (5)), 0 where w_t = 0 (reading R-19), NaN for a failed series.  Differences and products in
+// fp64; the band sum in band order.  One thread per (t, b); a block covers 256 series of rows
+// blockIdx.y, blockIdx.y + gridDim.y, ...
+template <typename IO>
+__global__ void grad_w_kernel(const IO* __restrict__ w, const IO* __restrict__ y, const IO* __restrict__ z,
+                              const IO* __restrict__ gy, const int32_t* __restrict__ info, IO* __restrict__ gw,
+                              long long T, long long B, int nb) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const bool failed = info[b] != 0;
+  const long long plane = T * B;
+  for (long long t = blockIdx.y; t < T; t += gridDim.y) {
+    const long long i = t * B + b;
+    const IO wt = w[i];
+    double acc = 0.0;
+    if (wt != IO(0)) {
+      const double wd = to_f64<IO>(wt);
+      for (int c = 0; c < nb; ++c) {
+        const long long j = c * plane + i;
+        acc = fma(to_f64<IO>(gy[j]) / wd, to_f64<IO>(y[j]) - to_f64<IO>(z[j]), acc);
+      }
+    }
+    gw[i] = from_f64<IO>(failed ? qnan() : acc);
+  }
+}
+
 // Count of failed series (info != 0) for whit_failures.
 __global__ void count_failures(const int32_t* __restrict__ info, long long B, unsigned long long* out) {
   unsigned long long n = 0;

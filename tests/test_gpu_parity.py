@@ -670,3 +670,69 @@ def test_s2tile_full_shape_sampled():
             assert ez <= tz, (b, c, ez)
             assert rel_series(yb[c], o["ybar"][c]).max() <= tg, (b, c)
         assert rel_series(gl[:, b].double().cpu().numpy(), o["lambar"]).max() <= tg, b
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_grad_w_vs_oracle(d, per_date, dtype):
+    """whit_grad_w (NEXT-3 option): dL/dw = u (y - z), 0 at w = 0 (R-19), vs O1.weight_grad on sampled
+    series (several tiles and a ragged warp), NaN-poisoned for failed series."""
+    import paper_2604_00048_b200 as P
+
+    T, B = 203, 300
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", dtype=dtype, seed=900 + d)
+    x["w"][:, 7] = 0.0  # a failed series
+    y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
+    ws = P.Workspace(d, T, B, dtype, per_date)
+    z, gy, gl, gw = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam), torch.empty_like(w)
+    P.whit_forward(y, w, lam, d, T, B, z, ws)
+    P.whit_backward(g, ws, z, gy, gl)
+    P.whit_grad_w(ws, y, z, gy, gw)
+    torch.cuda.synchronize()
+    gwn = gw.double().cpu().numpy()
+    assert np.all(np.isnan(gwn[:, 7]))
+    assert np.all(gwn[(w == 0).cpu().numpy() & ~np.isnan(gwn)] == 0)
+    tg = TOL[(dtype, d)][1] * (10 if d == 3 and dtype == torch.float32 else 1)
+    for b in (0, 1, 150, 299):
+        h = host_inputs({k: x[k][:, b] if x[k].dim() == 2 else x[k][b] for k in ("y", "w", "lam", "g")})
+        o = O1.forward_backward(h["y"], h["w"], h["lam"], d, h["g"])
+        ref = O1.weight_grad(h["y"], h["w"], o["z"], o["u"])
+        assert rel_series(gwn[:, b], ref).max() <= tg, b
+
+
+def test_grad_w_bands_and_autograd():
+    """Multi-band workspace: dL/dw sums u_c (y_c - z_c) over the bands (O1 bands oracle); and the autograd
+    shim returns w.grad equal to a direct whit_grad_w call, bit for bit."""
+    import paper_2604_00048_b200 as P
+
+    d, C, T, B = 2, 3, 150, 96
+    x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, device="cuda", seed=31)
+    y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
+    ws = P.Workspace(d, T, B, torch.float32, True, C=C)
+    z, gy, gl, gw = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam), torch.empty_like(w)
+    P.whit_forward_bands(y, w, lam, d, T, B, C, z, ws)
+    P.whit_backward_bands(g, ws, z, gy, gl)
+    P.whit_grad_w(ws, y, z, gy, gw)
+    torch.cuda.synchronize()
+    for b in (0, 50, 95):
+        Y, G = y[:, :, b].double().cpu().numpy(), g[:, :, b].double().cpu().numpy()
+        wb, lb = w[:, b].double().cpu().numpy(), lam[:, b].double().cpu().numpy()
+        o = O1.forward_backward_bands(Y, wb, lb, d, G)
+        ref = sum(O1.weight_grad(Y[c], wb, o["z"][c], o["u"][c]) for c in range(C))
+        assert rel_series(gw[:, b].double().cpu().numpy(), ref).max() <= 1e-3, b
+    # autograd: single band, B not a multiple of 4 (padded columns)
+    xs = synth.make_inputs("hetero", B=37, T=T, d=d, device="cuda", seed=32)
+    wr = xs["w"].clone().requires_grad_(True)
+    out = P.smooth(xs["y"], wr, xs["lam"], d)
+    out.backward(xs["g"])
+    ws1 = P.Workspace(d, T, 40, torch.float32, True)
+    pad = lambda a, v: torch.cat([a, torch.full((a.shape[0], 3), v, device="cuda", dtype=a.dtype)], 1).contiguous()
+    yp, wp, lp, gp = pad(xs["y"], 0.0), pad(xs["w"], 1.0), pad(xs["lam"], 1.0), pad(xs["g"], 0.0)
+    z1, gy1, gl1, gw1 = torch.empty_like(yp), torch.empty_like(yp), torch.empty_like(lp), torch.empty_like(wp)
+    P.whit_forward(yp, wp, lp, d, T, 40, z1, ws1)
+    P.whit_backward(gp, ws1, z1, gy1, gl1)
+    P.whit_grad_w(ws1, yp, z1, gy1, gw1)
+    torch.cuda.synchronize()
+    assert torch.equal(wr.grad, gw1[:, :37])
