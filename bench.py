@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="series in the CPU-oracle sample (0 = auto)")
+    ap.add_argument("--dist-smoke", action="store_true",
+                    help="initialise the NCCL process group even at world size 1 (under torchrun) so the "
+                         "barrier / all_reduce / all_gather paths of the multi-GPU run execute on one GPU")
     return ap.parse_args()
 
 
@@ -69,7 +72,7 @@ def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar over the default process group (identity without one)."""
     import torch
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -85,8 +88,8 @@ def gather_checksums(tensors, world: int) -> dict:
     sums = torch.stack([t.view(torch.int32 if t.element_size() == 4 else torch.int64).sum(dtype=torch.int64)
                         for t in tensors])
     allsums = [sums]
-    if world > 1:
-        allsums = [torch.empty_like(sums) for _ in range(world)]
+    if dist.is_available() and dist.is_initialized():
+        allsums = [torch.empty_like(sums) for _ in range(dist.get_world_size())]
         dist.all_gather(allsums, sums)
     return {"kind": "int64 sum of the output bit patterns (z, grad_y, grad_lambda) per rank",
             "per_rank": [[int(v) for v in a.tolist()] for a in allsums]}
@@ -295,11 +298,12 @@ def run_libwhit(args):
         if ws_n == 1 and args.gpus > 1:
             print(json.dumps({"error": f"--gpus {args.gpus} needs torchrun with {args.gpus} processes"}))
             return 2
-    if ws_n > 1:
+    if ws_n > 1 or args.dist_smoke:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if ws_n > 1 else 0)
     torch.cuda.set_device(dev)
+    distributed = dist.is_initialized()
 
     import paper_2604_00048_b200 as P
     import synth
@@ -340,7 +344,7 @@ def run_libwhit(args):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(dev.index if dev.index is not None else 0)
-    if ws_n > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize(dev)
     clk.start()
@@ -354,7 +358,7 @@ def run_libwhit(args):
         ev[i][2].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize(dev)
-    if ws_n > 1:
+    if distributed:
         dist.barrier()
     clocks = clk.stop()
     total_ms = t_start.elapsed_time(t_end)
@@ -452,7 +456,7 @@ def run_libwhit(args):
             "w_bits": wbits_line, "checksums": checksums,
         }
         print(json.dumps(line), flush=True)
-    if ws_n > 1:
+    if distributed:
         dist.destroy_process_group()
     return 0
 
@@ -608,8 +612,8 @@ def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6):
     buf = P.whit_run_host(h["y"], h["w"], h["lam"], h["g"], d, oz, oy, ol, chunk=chunk, nbuf=nbuf, stream=stream)
     torch.cuda.synchronize(dev)
     ws_n = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws_n > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_initialized():
         dist.barrier()  # ranks share the host's memory and PCIe: start the timed region together
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
