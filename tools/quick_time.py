@@ -7,7 +7,8 @@ import synth
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "hetero"
 dtype = torch.float64 if (len(sys.argv) > 2 and sys.argv[2] == "f64") else torch.float32
-x = synth.make_inputs(cfg, device="cuda", dtype=dtype)
+QB = int(os.environ.get("QT_B", "0")) or None  # override the batch (tail-effect experiments)
+x = synth.make_inputs(cfg, device="cuda", dtype=dtype, **({"B": QB} if QB else {}))
 y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
 T, B = y.shape
 d = 2
