@@ -174,14 +174,14 @@ whit_status whit_grad_w(whit_ws* factor_ws, const void* y, const void* z, const 
  *   lambda, grad_lambda    [T-d][B] or [B]  (shared; grad_lambda is summed over
  *                                             bands, in a fixed order, in fp64:
  *                                             dL/dlambda_r = -sum_c (D u_c)_r (D z_c)_r)
- * 1 <= C <= 10 for F32 planes, <= 5 for F64 (one CTA's shared memory holds the
- * C band pipelines).  The factor is formed once per pixel per sweep by one
- * factor warp and handed to the band warps through shared memory (two bands per
- * band warp), so w, lambda and factor-checkpoint bytes and the factor's fp64
- * work are amortised over C bands; every band's z and grad_y equal the
- * single-band results bit for bit.  The
- * single-band entry points above are the C = 1 case (whit_forward on a C > 1
- * workspace is WHIT_ERR_SHAPE; whit_backward works for any C). */
+ * 1 <= C <= 10 (one CTA's shared memory holds the C band pipelines).  The
+ * factor is formed once per pixel per sweep by one factor warp and handed to
+ * the band warps through shared memory (two bands per band warp), so w,
+ * lambda and factor-checkpoint bytes and the factor's fp64 work are amortised
+ * over C bands; every band's z and grad_y equal the single-band results bit
+ * for bit.  The single-band entry points above are the C = 1 case
+ * (whit_forward on a C > 1 workspace is WHIT_ERR_SHAPE; whit_backward works
+ * for any C). */
 size_t whit_ws_bytes_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype, whit_lambda_mode lambda_mode);
 
 whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,

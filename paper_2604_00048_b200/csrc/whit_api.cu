@@ -161,41 +161,52 @@ struct DeviceGuard {
 // Dynamic smem budget of one CTA (227 KB opt-in minus the kernel's static barriers).
 constexpr int kSmemBudget = 232448 - 2048;
 
-// Largest band count whose CTA fits shared memory, for every kernel of this dtype.
-template <typename IO>
-constexpr int max_bands_io() {
-  int m = whit::kMaxBands;
-  constexpr int w[] = {whit::Layout<1, IO, true, true>::WARP_SMEM, whit::Layout<2, IO, true, true>::WARP_SMEM,
-                       whit::Layout<3, IO, true, true>::WARP_SMEM, whit::Layout<1, IO, true, false>::WARP_SMEM,
-                       whit::Layout<2, IO, true, false>::WARP_SMEM, whit::Layout<3, IO, true, false>::WARP_SMEM};
-  for (int x : w) {
-    int nb = (kSmemBudget - 4096 - 8 * 32 * whit::kMaxBands) / x;
-    if (nb < m) m = nb;
-  }
+// Largest band count whose shared-factor CTA (whit_mb2_kernel) fits shared memory, for every
+// (d, lambda mode, direction) of this dtype.
+template <typename IO, int D, bool PD, bool BWD>
+constexpr int max_bands_mb2() {
+  int m = 0;
+  for (int nb = 1; nb <= whit::kMaxBands; ++nb)
+    if (whit::MB2Layout<D, IO, PD, BWD>::smem(nb) <= kSmemBudget) m = nb;
   return m;
 }
+template <typename IO, int D>
+constexpr int max_bands_d() {
+  const int v[] = {max_bands_mb2<IO, D, true, true>(), max_bands_mb2<IO, D, true, false>(),
+                   max_bands_mb2<IO, D, false, true>(), max_bands_mb2<IO, D, false, false>()};
+  int m = whit::kMaxBands;
+  for (int x : v) m = x < m ? x : m;
+  return m;
+}
+template <typename IO>
+constexpr int max_bands_io() {
+  const int v[] = {max_bands_d<IO, 1>(), max_bands_d<IO, 2>(), max_bands_d<IO, 3>()};
+  int m = whit::kMaxBands;
+  for (int x : v) m = x < m ? x : m;
+  return m;
+}
+static_assert(max_bands_io<float>() == whit::kMaxBands && max_bands_io<double>() == whit::kMaxBands,
+              "every multi-band kernel fits kMaxBands bands in one CTA");
 int max_bands(whit_dtype dt) { return dt == WHIT_F32 ? max_bands_io<float>() : max_bands_io<double>(); }
 
-template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false, bool WB = false>
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
 whit_status launch(const Params& p, cudaStream_t s) {
   using L = whit::Layout<D, IO, PD, BWD, LOSS, WB>;
-  constexpr int max_smem = MB ? L::smem_mb(max_bands_io<IO>()) : L::SMEM;
+  constexpr int max_smem = L::SMEM;
   static_assert(max_smem <= kSmemBudget, "CTA shared memory over budget");
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS, WB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, LOSS, WB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, MB, LOSS, WB>,
+    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, LOSS, WB>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
   });
   if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  // one pixel per thread, one TMA pipeline per warp
-  const int threads = MB ? 32 * p.nb : 32 * L::WARPS;
-  const long long per_cta = MB ? 32 : threads;
-  const long long grid = (p.B + per_cta - 1) / per_cta;
-  const int smem = MB ? L::smem_mb(p.nb) : L::SMEM;
-  whit::whit_kernel<D, IO, PD, BWD, MB, LOSS, WB><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
+  // one series per thread, one TMA pipeline per warp
+  const int threads = 32 * L::WARPS;
+  const long long grid = (p.B + threads - 1) / threads;
+  whit::whit_kernel<D, IO, PD, BWD, LOSS, WB><<<dim3((unsigned)grid), dim3(threads), L::SMEM, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
@@ -237,9 +248,9 @@ whit_status dispatch_d(int d, const Params& p, cudaStream_t s) {
     return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
   } else {
   switch (d) {
-    case 1: return launch<1, IO, PD, BWD, MB>(p, s);
-    case 2: return launch<2, IO, PD, BWD, MB>(p, s);
-    case 3: return launch<3, IO, PD, BWD, MB>(p, s);
+    case 1: return launch<1, IO, PD, BWD>(p, s);
+    case 2: return launch<2, IO, PD, BWD>(p, s);
+    case 3: return launch<3, IO, PD, BWD>(p, s);
   }
   return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
   }
@@ -254,9 +265,9 @@ whit_status dispatch_pd(const whit_ws* ws, const Params& p) {
 template <typename IO, bool PD, bool BWD>
 whit_status dispatch_wb_d(int d, const Params& p, cudaStream_t s) {
   switch (d) {
-    case 1: return launch<1, IO, PD, BWD, false, false, true>(p, s);
-    case 2: return launch<2, IO, PD, BWD, false, false, true>(p, s);
-    case 3: return launch<3, IO, PD, BWD, false, false, true>(p, s);
+    case 1: return launch<1, IO, PD, BWD, false, true>(p, s);
+    case 2: return launch<2, IO, PD, BWD, false, true>(p, s);
+    case 3: return launch<3, IO, PD, BWD, false, true>(p, s);
   }
   return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
 }
@@ -280,9 +291,9 @@ whit_status dispatch(const whit_ws* ws, const Params& p) {
 template <typename IO, bool PD>
 whit_status dispatch_loss_d(int d, const Params& p, cudaStream_t s) {
   switch (d) {
-    case 1: return launch<1, IO, PD, false, false, true>(p, s);
-    case 2: return launch<2, IO, PD, false, false, true>(p, s);
-    case 3: return launch<3, IO, PD, false, false, true>(p, s);
+    case 1: return launch<1, IO, PD, false, true>(p, s);
+    case 2: return launch<2, IO, PD, false, true>(p, s);
+    case 3: return launch<3, IO, PD, false, true>(p, s);
   }
   return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
 }

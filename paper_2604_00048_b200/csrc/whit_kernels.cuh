@@ -64,7 +64,7 @@ struct Params {
   CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
   void* loss;             // LOSS: per-series loss [B]
   const uint32_t* wbits;  // WB: bit-packed 0/1 weights [ceil(T/32)][B], bit t%32 of word t/32
-  double* ck_fac;         // factor checkpoints [C][NFAC][B] (written by band 0, read by all bands)
+  double* ck_fac;         // factor checkpoints [C][NFAC][B] (forward up sweep; read by every later sweep)
   double* ck_rhs_f;       // forward rhs checkpoints [C][nb][d][B]
   double* ck_rhs_b;       // backward rhs checkpoints [C][nb][d][B]
   int32_t* info;          // [B]
@@ -288,8 +288,6 @@ template <int D> struct Ck {
 // more staged plane, 21 KB per warp): 2-warp CTAs at <= 200 regs (8 warps/SM);
 // ncu shows both DRAM-bound (~6.0 TB/s), and staging the backward's outputs in
 // place to reach 12 warps measured no faster (slower on small batches).
-// Multi-band (MB): one CTA = nb warps (one band each) over the same 32 pixels,
-// <= 168 regs so that up to 12 warps fit one CTA.
 #ifndef WHIT_TILE_K2
 #define WHIT_TILE_K2 16
 #endif
@@ -307,7 +305,6 @@ template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int ST = 2;
   static constexpr int WARPS = BWD ? WHIT_BWD_WARPS : 4;
   static constexpr int MAXREG = BWD ? WHIT_BWD_MAXREG : WHIT_FWD_MAXREG;  // SMSP register files (16K): 3 warps/SMSP need <= 168
-  static constexpr int MB_MAXREG = 168;  // registers are granted per 4 warps: 12 x 32 x 168 <= 64K
 };
 constexpr int kMaxBands = 10;
 
@@ -328,8 +325,6 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   static constexpr bool DIRECT = false;  // measured: no gain over TMA-staged stores at 8 warps (DRAM/power-bound), homo slower
   static constexpr int WARP_SMEM = ST * STAGE + ((INPLACE || DIRECT) ? 0 : (LOSS ? 3 : 2) * OUT);
   static constexpr int SMEM = WARPS * WARP_SMEM;
-  // multi-band CTA of nb warps: rings + reduction tile + scalar slots
-  static constexpr int smem_mb(int nb) { return nb * WARP_SMEM + OUT + nb * 32 * 8; }
   static constexpr uint32_t BYTES_UP = ((WB ? 1 : 2) * K + (PD ? K : 0)) * ROW;
   static constexpr uint32_t BYTES_DN = ((WB ? 1 : 2) * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
 };
@@ -533,32 +528,27 @@ struct Sweep {
 };
 
 // ------------------------------------------------------------------ the kernel
-// One launch = one full forward (BWD=false) or backward (BWD=true).  Each
-// warp owns 32 consecutive pixels x one band and its own TMA ring: up sweep
-// over C chunks, then down sweep over C chunks in reverse.
-//   MB = false: independent series (nb = 1), WARPS independent warps per CTA.
-//   MB = true : CTA = nb warps, one per band of the same 32 pixels; they share
-//               the factor (band 0 writes its checkpoints, every band reads
-//               them) and, in the backward, reduce -(Du_c)(Dz_c) over bands in
-//               shared memory in band order (deterministic).
-template <int D, typename IO, bool PD, bool BWD, bool MB, bool LOSS = false, bool WB = false>
-__global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Tile<IO, D, BWD>::MAXREG))
-    whit_kernel(const __grid_constant__ Params p) {
-  static_assert(!LOSS || (!BWD && !MB), "the fused loss is a single-band forward variant");
-  static_assert(!WB || (!MB && !LOSS), "bit-packed W is a single-band fwd/bwd variant");
+// One launch = one full forward (BWD=false) or backward (BWD=true) of independent series.  Each
+// warp owns 32 consecutive series (one per lane) and its own TMA ring: up sweep over C chunks,
+// then down sweep over C chunks in reverse; WARPS independent warps per CTA.  (Multi-band
+// pixels sharing a factor use whit_mb2_kernel, whit_mb2.cuh.)
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
+__global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid_constant__ Params p) {
+  static_assert(!LOSS || !BWD, "the fused loss is a forward variant");
+  static_assert(!WB || !LOSS, "bit-packed W is a fwd/bwd variant");
   using L = Layout<D, IO, PD, BWD, LOSS, WB>;
   using S = Sweep<D, IO, PD, BWD, LOSS, WB>;
   constexpr int K = L::K, ST = L::ST;
   constexpr int NFAC = Ck<D>::NFAC;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[MB ? kMaxBands : L::WARPS][ST];
+  __shared__ __align__(8) uint64_t full_bar[L::WARPS][ST];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = p.T, C = p.C, nb = MB ? p.nb : 1;
+  const int T = p.T, C = p.C, nb = 1;
   const long long B = p.B;
-  const int band = MB ? warp : 0;
-  const long long bw = MB ? (long long)blockIdx.x * 32 : ((long long)blockIdx.x * L::WARPS + warp) * 32;
-  if (bw >= B) return;  // (MB: the whole CTA) past the end; no barrier follows for these warps
+  const int band = 0;
+  const long long bw = ((long long)blockIdx.x * L::WARPS + warp) * 32;
+  if (bw >= B) return;  // past the end; no barrier follows for these warps
   const long long b = bw + lane;
   const bool valid = b < B;
   unsigned char* ring = smem + warp * L::WARP_SMEM;
@@ -567,9 +557,6 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
   IO* so2 = reinterpret_cast<IO*>(ring + ST * L::STAGE + 2 * L::OUT);  // LOSS only
   uint64_t* bars = full_bar[warp];
   const int ntiles = 2 * C;
-  // MB backward: per-CTA reduction tile (K rows x 32 pixels) and scalar slots
-  IO* red = reinterpret_cast<IO*>(smem + (MB ? nb : 0) * L::WARP_SMEM);
-  double* redS = reinterpret_cast<double*>(smem + (MB ? nb : 0) * L::WARP_SMEM + L::OUT);
 
   if (lane == 0) {
 #pragma unroll
@@ -607,7 +594,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     const unsigned char* stg = ring + s * L::STAGE;
     const int t0 = c * K;
     if (valid) {  // checkpoint: state entering row t0
-      if (!BWD && band == 0) {
+      if (!BWD) {
         double* ck = p.ck_fac + (long long)c * NFAC * B + b;
         int f = 0;
 #pragma unroll
@@ -626,8 +613,8 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
     else S::template up_chunk<true>(st, stg, lane, t0, T, lam_s, nobs, pos, wm);
     if (WB && !BWD) nobs += __popc(wm);  // bits past T are 0 (packing)
     allpos = allpos && pos;
-    // exact failing row (cold): band 0 only -- it wrote the factor checkpoint it replays from
-    if (!BWD && !pos && bad == 0 && valid && band == 0) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s, wm);
+    // exact failing row (cold path): replayed from the factor checkpoint this warp wrote
+    if (!BWD && !pos && bad == 0 && valid) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s, wm);
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
@@ -639,17 +626,14 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
   // singular for lambda > 0); else first non-positive pivot row.  A failed
   // series is poisoned with NaN in the restored rhs state, so every output
   // derived from it (z, D z, w*u, -(D u)(D z)) is NaN without per-store checks.
-  // All bands of a pixel compute the identical factor, hence the same status.
   bool failed;
   if (!BWD) {
-    if (valid && band == 0) p.info[b] = (nobs < D) ? (T - D + 1) : bad;
+    if (valid) p.info[b] = (nobs < D) ? (T - D + 1) : bad;
     failed = (nobs < D) || !allpos;
   } else {
     failed = valid ? (p.info[b] != 0) : true;
   }
   const double poison = failed ? qnan() : 0.0;
-  // MB: band 0's factor checkpoints (global) become visible to the other bands' down sweeps
-  if (MB) __syncthreads();
 
   // ================================================================ down sweep
   double cA[D][D];  // A[t0+K+i][j+1] of the chunk processed before (later in time)
@@ -728,29 +712,9 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
       tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
       if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
       if (LOSS) tma_store_3d(&p.tm_out2, so2, (int)bw, t0, 0);
-      if (BWD && PD && !MB) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
+      if (BWD && PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
       bulk_commit();
     }
-    if (MB && BWD && PD) {
-      // grad_lambda_r = sum over bands of -(D u_c)_r (D z_c)_r, summed in band order in fp64
-      if (threadIdx.x == 0) bulk_wait_read0();  // previous reduced tile has been read by its store
-      __syncthreads();
-      for (int k = warp; k < K; k += nb) {
-        double acc = 0.0;
-        for (int cb = 0; cb < nb; ++cb)
-          acc += to_f64<IO>(reinterpret_cast<const IO*>(smem + cb * L::WARP_SMEM +
-                                                        (L::INPLACE ? s * L::STAGE + L::OFF_DZ
-                                                                    : ST * L::STAGE + L::OUT))[k * 32 + lane]);
-        red[k * 32 + lane] = from_f64<IO>(acc);
-      }
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tma_store_2d(&p.tm_out1, red, (int)bw, t0);
-        bulk_commit();
-      }
-    }
-
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       if (L::INPLACE) bulk_wait_read0();  // the stores read this very stage
@@ -761,19 +725,7 @@ __global__ void __maxnreg__((MB ? Tile<IO, D, BWD>::MB_MAXREG : LOSS ? 200 : Til
 #undef WHIT_LOAD_CK
   if (lane == 0) bulk_wait0();  // stores complete before the CTA exits (smem stays valid)
   if (LOSS && valid) reinterpret_cast<IO*>(p.loss)[b] = from_f64<IO>(lam_acc / (double)T);
-  if (BWD && !PD) {
-    if (MB) {  // scalar lambda: reduce the per-band sums in band order
-      redS[warp * 32 + lane] = lam_acc;
-      __syncthreads();
-      if (warp == 0) {
-        double acc = 0.0;
-        for (int cb = 0; cb < nb; ++cb) acc += redS[cb * 32 + lane];
-        if (valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(acc);
-      }
-    } else if (valid) {
-      reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc);
-    }
-  }
+  if (BWD && !PD && valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc);
 }
 
 // ------------------------------------------------------------------ irregular grid (NEXT-2)

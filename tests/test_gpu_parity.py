@@ -293,8 +293,6 @@ def test_bands_shared_factor(d, C, per_date, dtype):
     """NEXT-1: C bands per pixel sharing w and lambda; per band vs O2 (band-series with the pixel's
     w, lambda), lambda gradient = sum over bands (oracle O1 forward_backward_bands on a subsample)."""
     T, B = 203, 300
-    if dtype == torch.float64:
-        C = min(C, 5)  # fp64 planes: 5 band warps fill a CTA's shared memory
     x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
                                 device="cuda", dtype=dtype, seed=500 + d * 10 + C)
     res = run_cuda_bands(x, d, C, dtype)
@@ -344,14 +342,14 @@ def test_bands_one_equals_single_series_path():
 
 
 def test_bands_limits():
-    """C is capped at 10 (f32) / 5 (f64): one CTA's shared memory holds the C band pipelines."""
+    """C is capped at 10 for both dtypes (kMaxBands: one shared-factor CTA holds 5 band warps)."""
     import paper_2604_00048_b200 as P
     P.Workspace(2, 100, 128, torch.float32, True, C=10)
-    P.Workspace(2, 100, 128, torch.float64, True, C=5)
+    P.Workspace(2, 100, 128, torch.float64, True, C=10)
     with pytest.raises(P.WhitError):
         P.Workspace(2, 100, 128, torch.float32, True, C=11)
     with pytest.raises(P.WhitError):
-        P.Workspace(2, 100, 128, torch.float64, True, C=6)
+        P.Workspace(2, 100, 128, torch.float64, True, C=11)
 
 
 def run_cuda_var(x: dict, d: int, dtype):
