@@ -204,7 +204,13 @@ whit_status whit_backward_bands(const void* grad_z, whit_ws* factor_ws, const vo
  * Workspace from whit_ws_create_times (checkpoint interval 8); the matching
  * backward is whit_backward (the workspace remembers times, which must stay
  * valid and unmodified until it has run).  info: T-d+1 (< d observed days),
- * -1 (other non-positive pivot).  Single band.  One launch each. */
+ * -1 (other non-positive pivot).  One launch each.
+ * The _bands variants take C <= 10 bands per pixel sharing w, lambda and
+ * times (the paper's Table 1 workload: C = 10 on uneven dates),
+ * with the multi-band layout above (y, z, grad_z, grad_y [C][T][B]); one
+ * factor per pixel (the shared-factor kernel with the per-row dates stencils);
+ * every band's z and grad_y equal the single-band irregular results bit for
+ * bit, grad_lambda is summed over bands.  whit_forward_times is C = 1. */
 size_t whit_ws_bytes_times(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode);
 
 whit_status whit_ws_create_times(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
@@ -213,6 +219,16 @@ whit_status whit_ws_create_times(whit_ws** out, int d, int64_t T, int64_t B, whi
 
 whit_status whit_forward_times(const void* y, const void* w, const void* lambda, const void* times, int d,
                                int64_t T, int64_t B, void* z, whit_ws* factor_ws);
+
+size_t whit_ws_bytes_times_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                                 whit_lambda_mode lambda_mode);
+
+whit_status whit_ws_create_times_bands(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                                       whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes,
+                                       void* cuda_stream);
+
+whit_status whit_forward_times_bands(const void* y, const void* w, const void* lambda, const void* times, int d,
+                                     int64_t T, int64_t B, int C, void* z, whit_ws* factor_ws);
 
 /* ---------------------------------------------------------------------------
  * Bit-packed W.  The paper's W is binary (w_ii is 1 if the date was

@@ -48,6 +48,11 @@ SIGNATURES = [
     ("whit_ws_create_times", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                             _VP, _SZ, _VP]),
     ("whit_forward_times", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
+    ("whit_ws_bytes_times_bands", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("whit_ws_create_times_bands", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int,
+                                                  ctypes.c_int, ctypes.c_int, _VP, _SZ, _VP]),
+    ("whit_forward_times_bands", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, _VP,
+                                                _VP]),
     ("whit_pack_mask", ctypes.c_int, [_VP, _I64, _I64, ctypes.c_int, _VP, _VP]),
     ("whit_forward_wbits", ctypes.c_int, [_VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP]),
     ("whit_forward_mse", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, _VP, _VP, _VP, _VP]),
@@ -122,7 +127,7 @@ class Workspace:
     def __init__(self, d: int, T: int, B: int, dtype: torch.dtype, per_date: bool, device=None, stream=None,
                  C: int = 1, times: bool = False):
         if times:
-            nbytes = int(_lib.whit_ws_bytes_times(d, T, B, _dtype_code(dtype), int(per_date)))
+            nbytes = int(_lib.whit_ws_bytes_times_bands(d, T, B, C, _dtype_code(dtype), int(per_date)))
         else:
             nbytes = whit_ws_bytes_bands(d, T, B, C, dtype, per_date)
         if nbytes == 0:
@@ -131,9 +136,10 @@ class Workspace:
         self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
         h = ctypes.c_void_p()
         if times:
-            _check(_lib.whit_ws_create_times(ctypes.byref(h), d, T, B, _dtype_code(dtype), int(per_date),
-                                             ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
-                   "whit_ws_create_times")
+            _check(_lib.whit_ws_create_times_bands(ctypes.byref(h), d, T, B, C, _dtype_code(dtype), int(per_date),
+                                                   ctypes.c_void_p(self.buf.data_ptr()), nbytes,
+                                                   _stream_handle(stream)),
+                   "whit_ws_create_times_bands")
         else:
             _check(_lib.whit_ws_create_bands(ctypes.byref(h), d, T, B, C, _dtype_code(dtype), int(per_date),
                                              ctypes.c_void_p(self.buf.data_ptr()), nbytes, _stream_handle(stream)),
@@ -175,6 +181,12 @@ def whit_grad_w(ws: Workspace, y, z, grad_y, grad_w):
 def whit_forward_times(y, w, lam, times, d: int, T: int, B: int, z, ws: Workspace):
     _check(_lib.whit_forward_times(_ptr(y), _ptr(w), _ptr(lam), _ptr(times), d, T, B, _ptr(z), ws.handle),
            "whit_forward_times")
+
+
+def whit_forward_times_bands(y, w, lam, times, d: int, T: int, B: int, C: int, z, ws: Workspace):
+    """C bands per pixel on uneven dates (y, z: [C][T][B]; w, lam, times shared)."""
+    _check(_lib.whit_forward_times_bands(_ptr(y), _ptr(w), _ptr(lam), _ptr(times), d, T, B, C, _ptr(z), ws.handle),
+           "whit_forward_times_bands")
 
 
 def whit_pack_mask(w, bits=None, stream=None):

@@ -10,7 +10,8 @@ scalar per series), CUDA, contiguous, float32 or float64.  Variants:
 
 * ``y`` of shape ``(C, T, B)``: C bands per pixel sharing ``w`` and ``lam``
   (``whit_forward_bands``, NEXT-1); ``lam``'s gradient is summed over bands;
-* ``times=(T, B)``: uneven acquisition dates (``whit_forward_times``, NEXT-2).
+* ``times=(T, B)``: uneven acquisition dates (``whit_forward_times``, NEXT-2; with bands:
+  ``whit_forward_times_bands``).
 
 ``w`` gets a gradient when it requires one: ``dL/dw_t = sum_c u_t (y_t - z_t)`` (``whit_grad_w``; 0 at
 ``w_t = 0``, reading R-19).
@@ -46,8 +47,8 @@ class WhittakerFn(torch.autograd.Function):
             raise ValueError(f"scalar lambda must be (B,), got {tuple(lam.shape)}")
         if not (y.dtype == w.dtype == lam.dtype):
             raise TypeError("y, w, lambda must share a dtype")
-        if times is not None and (bands or times.shape != (T, B) or times.dtype != y.dtype):
-            raise ValueError("times must be (T, B) of y's dtype (single band)")
+        if times is not None and (times.shape != (T, B) or times.dtype != y.dtype):
+            raise ValueError("times must be (T, B) of y's dtype")
         q = 4 if y.dtype == torch.float32 else 2
         Bp = (B + q - 1) // q * q  # 16-byte row stride; padded series: w = 1, lam = 1, y = 0
         yp = _pad_cols(y, Bp, 0.0)
@@ -58,8 +59,11 @@ class WhittakerFn(torch.autograd.Function):
             tp = times if Bp == B else torch.cat(
                 [times, torch.arange(T, dtype=times.dtype, device=times.device)[:, None].expand(T, Bp - B)], dim=1)
             tp = tp.contiguous()
-            ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device, times=True)
-            L.whit_forward_times(yp, wp, lp, tp, d, T, Bp, z, ws)
+            ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device, C=C, times=True)
+            if bands:
+                L.whit_forward_times_bands(yp, wp, lp, tp, d, T, Bp, C, z, ws)
+            else:
+                L.whit_forward_times(yp, wp, lp, tp, d, T, Bp, z, ws)
             keep = (wp, lp, z, tp)
         elif bands:
             ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device, C=C)

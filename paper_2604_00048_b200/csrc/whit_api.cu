@@ -167,7 +167,9 @@ template <typename IO, int D, bool PD, bool BWD>
 constexpr int max_bands_mb2() {
   int m = 0;
   for (int nb = 1; nb <= whit::kMaxBands; ++nb)
-    if (whit::MB2Layout<D, IO, PD, BWD>::smem(nb) <= kSmemBudget) m = nb;
+    if (whit::MB2Layout<D, IO, PD, BWD>::smem(nb) <= kSmemBudget &&
+        whit::MB2Layout<D, IO, PD, BWD, true>::smem(nb) <= kSmemBudget)
+      m = nb;
   return m;
 }
 template <typename IO, int D>
@@ -212,17 +214,18 @@ whit_status launch(const Params& p, cudaStream_t s) {
   return WHIT_OK;
 }
 
-// Multi-band with a shared factor warp (NEXT-1): CTA = nb band warps + 1 factor warp.
-template <int D, typename IO, bool PD, bool BWD>
+// Multi-band with a shared factor warp (NEXT-1): CTA = nb band warps + 1 factor warp (IRR: on
+// uneven acquisition dates, NEXT-2).
+template <int D, typename IO, bool PD, bool BWD, bool IRR = false>
 whit_status launch_mb2(const Params& p, cudaStream_t s) {
-  using L = whit::MB2Layout<D, IO, PD, BWD>;
+  using L = whit::MB2Layout<D, IO, PD, BWD, IRR>;
   constexpr int max_smem = L::smem(whit::kMaxBands);
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD, IRR>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          (int)cudaSharedmemCarveoutMaxShared);
-    attr_err = cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD>,
+    attr_err = cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD, IRR>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     max_smem < kSmemBudget ? max_smem : kSmemBudget);
   });
@@ -231,7 +234,7 @@ whit_status launch_mb2(const Params& p, cudaStream_t s) {
   if (smem > kSmemBudget) return fail(WHIT_ERR_SHAPE, "%d bands need %d B of shared memory", p.nb, smem);
   const long long grid = (p.B + 31) / 32;
   const int threads = 32 * (L::nwarps(p.nb) + 1);
-  whit::whit_mb2_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
+  whit::whit_mb2_kernel<D, IO, PD, BWD, IRR><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
@@ -376,7 +379,15 @@ whit_status launch_irr(const Params& p, cudaStream_t s) {
 }
 
 template <typename IO, bool PD, bool BWD>
-whit_status dispatch_irr_d(int d, const Params& p, cudaStream_t s) {
+whit_status dispatch_irr_d(int d, bool mb, const Params& p, cudaStream_t s) {
+  if (mb) {  // C > 1 bands on the uneven grid: shared-factor kernel with the dates stencils
+    switch (d) {
+      case 1: return launch_mb2<1, IO, PD, BWD, true>(p, s);
+      case 2: return launch_mb2<2, IO, PD, BWD, true>(p, s);
+      case 3: return launch_mb2<3, IO, PD, BWD, true>(p, s);
+    }
+    return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+  }
   switch (d) {
     case 1: return launch_irr<1, IO, PD, BWD>(p, s);
     case 2: return launch_irr<2, IO, PD, BWD>(p, s);
@@ -387,10 +398,12 @@ whit_status dispatch_irr_d(int d, const Params& p, cudaStream_t s) {
 
 template <bool BWD>
 whit_status dispatch_irr(const whit_ws* ws, const Params& p) {
-  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE, mb = ws->nb > 1;
   if (ws->dt == WHIT_F32)
-    return pd ? dispatch_irr_d<float, true, BWD>(ws->d, p, ws->stream) : dispatch_irr_d<float, false, BWD>(ws->d, p, ws->stream);
-  return pd ? dispatch_irr_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_irr_d<double, false, BWD>(ws->d, p, ws->stream);
+    return pd ? dispatch_irr_d<float, true, BWD>(ws->d, mb, p, ws->stream)
+              : dispatch_irr_d<float, false, BWD>(ws->d, mb, p, ws->stream);
+  return pd ? dispatch_irr_d<double, true, BWD>(ws->d, mb, p, ws->stream)
+            : dispatch_irr_d<double, false, BWD>(ws->d, mb, p, ws->stream);
 }
 
 }  // namespace
@@ -433,11 +446,22 @@ whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int
   return ws_create(out, d, T, B, C, dtype, lambda_mode, dev_buf, dev_bytes, cuda_stream, false);
 }
 
-size_t whit_ws_bytes_times(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode) {
+size_t whit_ws_bytes_times_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                                 whit_lambda_mode lambda_mode) {
   WsLayout L;
   if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE) return 0;
-  if (!layout(d, T, B, 1, dtype, &L, 8)) return 0;
+  if (!layout(d, T, B, C, dtype, &L, 8)) return 0;
   return L.total;
+}
+
+size_t whit_ws_bytes_times(int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode) {
+  return whit_ws_bytes_times_bands(d, T, B, 1, dtype, lambda_mode);
+}
+
+whit_status whit_ws_create_times_bands(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
+                                       whit_lambda_mode lambda_mode, void* dev_buf, size_t dev_bytes,
+                                       void* cuda_stream) {
+  return ws_create(out, d, T, B, C, dtype, lambda_mode, dev_buf, dev_bytes, cuda_stream, true);
 }
 
 whit_status whit_ws_create_times(whit_ws** out, int d, int64_t T, int64_t B, whit_dtype dtype,
@@ -571,14 +595,14 @@ whit_status whit_pack_mask(const void* w, int64_t T, int64_t B, whit_dtype dtype
   return WHIT_OK;
 }
 
-whit_status whit_forward_times(const void* y, const void* w, const void* lambda, const void* times, int d, int64_t T,
-                               int64_t B, void* z, whit_ws* ws) {
+whit_status whit_forward_times_bands(const void* y, const void* w, const void* lambda, const void* times, int d,
+                                     int64_t T, int64_t B, int C, void* z, whit_ws* ws) {
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
-  if (!ws->irr) return fail(WHIT_ERR_STATE, "workspace not created by whit_ws_create_times");
+  if (!ws->irr) return fail(WHIT_ERR_STATE, "workspace not created by whit_ws_create_times(_bands)");
   if (!y || !w || !lambda || !times || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
-  if (d != ws->d || T != ws->T || B != ws->B)
-    return fail(WHIT_ERR_SHAPE, "(d,T,B) = (%d,%lld,%lld) != workspace (%d,%lld,%lld)", d, (long long)T,
-                (long long)B, ws->d, (long long)ws->T, (long long)ws->B);
+  if (d != ws->d || T != ws->T || B != ws->B || C != ws->nb)
+    return fail(WHIT_ERR_SHAPE, "(d,T,B,C) = (%d,%lld,%lld,%d) != workspace (%d,%lld,%lld,%d)", d, (long long)T,
+                (long long)B, C, ws->d, (long long)ws->T, (long long)ws->B, ws->nb);
   if (!aligned16(y) || !aligned16(w) || !aligned16(lambda) || !aligned16(times) || !aligned16(z))
     return fail(WHIT_ERR_ALIGN, "data pointers must be 16-B aligned");
   if (z == y || z == w || z == lambda || z == times) return fail(WHIT_ERR_ARG, "z aliases an input");
@@ -588,8 +612,10 @@ whit_status whit_forward_times(const void* y, const void* w, const void* lambda,
   whit_status st = fill_params(ws, &p, y, w, lambda);
   if (st != WHIT_OK) return st;
   const int kK = ws->kk;
-  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
+  p.out0 = z;  // multi-band kernel: direct stores
+  p.out1 = ws->buf + ws->L.off_dz;
+  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
+  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
   if ((st = encode_map(&p.tm_lw, times, ws->dt, B, T, kK + 2 * d)) != WHIT_OK) return st;
   ws->have_fwd = false;
   st = dispatch_irr<false>(ws, p);
@@ -597,6 +623,11 @@ whit_status whit_forward_times(const void* y, const void* w, const void* lambda,
   ws->have_fwd = true;
   ws->w = w; ws->lam = lambda; ws->z = z; ws->times = times;
   return WHIT_OK;
+}
+
+whit_status whit_forward_times(const void* y, const void* w, const void* lambda, const void* times, int d, int64_t T,
+                               int64_t B, void* z, whit_ws* ws) {
+  return whit_forward_times_bands(y, w, lambda, times, d, T, B, 1, z, ws);
 }
 
 whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, const void* loss_w, int d, int64_t T,

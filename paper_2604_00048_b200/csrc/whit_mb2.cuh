@@ -22,7 +22,7 @@
 
 namespace whit {
 
-template <int D, typename IO, bool PD, bool BWD>
+template <int D, typename IO, bool PD, bool BWD, bool IRR = false>
 struct MB2Layout {
 #ifndef WHIT_MB2_K
 #define WHIT_MB2_K 8
@@ -33,18 +33,23 @@ struct MB2Layout {
   // rows per chunk; TMA ring slots (ST - 1 chunks of loads in flight per warp); bands per band warp
   static constexpr int K = WHIT_MB2_K, ST = WHIT_MB2_ST, BPW = 2;
   static constexpr int ROW = 32 * (int)sizeof(IO);
-  // factor warp ring: w K rows + lambda K+d rows
+  // factor warp ring: w K rows | lambda K (+d) rows | IRR: acquisition dates K+2d rows (t0-d .. t0+K+d-1)
   static constexpr int F_OFF_W = 0, F_OFF_LAM = K * ROW;
-  static constexpr int F_STAGE = (F_OFF_LAM + (PD ? (K + D) * ROW : 0) + 127) / 128 * 128;
+  static constexpr int F_OFF_TT = F_OFF_LAM + (PD ? (K + D) * ROW : 0);
+  static constexpr int F_STAGE = (F_OFF_TT + (IRR ? (K + 2 * D) * ROW : 0) + 127) / 128 * 128;
   // band warp ring stage: rhs K rows for each of its bands
   static constexpr int B_STAGE = BPW * K * ROW;
   static constexpr int B_WARP = ST * B_STAGE;
-  // factor buffer: per row k: A[k][0..D-1], iD[k] (fp64), w[k] (IO), lane-contiguous
-  static constexpr int FB_A = 0, FB_ID = D * K * 32 * 8, FB_W = (D + 1) * K * 32 * 8;
+  // factor buffer, lane-contiguous fp64 rows: A[k][0..d-1], 1/D[k]; IRR also the normalised stencils
+  // mu of rows t0-d .. t0+K-1 ([K+d][d], R-18) and c_{t,0} [K]; then w[k] (IO)
+  static constexpr int FB_A = 0, FB_ID = D * K * 32 * 8;
+  static constexpr int FB_MU = FB_ID + K * 32 * 8;
+  static constexpr int FB_C0 = FB_MU + (IRR ? (K + D) * D * 32 * 8 : 0);
+  static constexpr int FB_W = FB_C0 + (IRR ? K * 32 * 8 : 0);
   static constexpr int FBUF = (FB_W + K * 32 * (int)sizeof(IO) + 127) / 128 * 128;
-  static constexpr uint32_t F_BYTES_UP = (K + (PD ? K : 0)) * ROW;
-  static constexpr uint32_t F_BYTES_DN = (K + (PD ? K + D : 0)) * ROW;
-  // smem: factor ring | factor buffers x2 | band warps | per-warp reduction rows (fp64) + scalars
+  static constexpr uint32_t F_BYTES_UP = (K + (PD ? K : 0) + (IRR ? K + 2 * D : 0)) * ROW;
+  static constexpr uint32_t F_BYTES_DN = (K + (PD ? K + D : 0) + (IRR ? K + 2 * D : 0)) * ROW;
+  // smem: factor ring | factor buffers | band warps | per-warp reduction rows (fp64) + scalars
   static constexpr int OFF_FB = ST * F_STAGE;
   // factor buffers in flight: enough that the factor warp runs ahead of the band warps' jitter
   static constexpr int NFB = (BWD && PD) ? 3 : 4;
@@ -59,9 +64,9 @@ struct MB2Layout {
 #ifndef WHIT_MB2_MAXREG
 #define WHIT_MB2_MAXREG 168
 #endif
-template <int D, typename IO, bool PD, bool BWD>
+template <int D, typename IO, bool PD, bool BWD, bool IRR = false>
 __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_constant__ Params p) {
-  using L = MB2Layout<D, IO, PD, BWD>;
+  using L = MB2Layout<D, IO, PD, BWD, IRR>;
   constexpr int K = L::K, ST = L::ST, NFAC = Ck<D>::NFAC, NW = Newton<IO>::N, BPW = L::BPW;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t f_full[ST];
@@ -109,16 +114,43 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
         if (up) tma_load_2d(stg + L::F_OFF_LAM, &p.tm_lam_up, (int)bw, t0, &f_full[i % ST]);
         else tma_load_2d(stg + L::F_OFF_LAM, &p.tm_lam_dn, (int)bw, t0 - D, &f_full[i % ST]);
       }
+      if (IRR) tma_load_2d(stg + L::F_OFF_TT, &p.tm_lw, (int)bw, t0 - D, &f_full[i % ST]);  // dates
     };
     if (lane == 0)
       for (int i = 0; i < ST && i < ntiles; ++i) issue(i);
     __syncwarp();
     const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
-    FState<D> st;
+    IState<D> S;  // factor recurrence state (S.mu: stencils of the last d columns, IRR only)
+    FState<D>& st = S.f;
     state_init<D>(st);
+#pragma unroll
+    for (int i = 0; i < D; ++i) binomial_col<D>(S.mu[i]);
     int nobs = 0;
     bool allpos = true;
     int it = 0, fb = 0;  // fb: factor-buffer sequence number
+    // one factor row: daily grid (ldl_step, binomial stencil) or uneven dates (R-18: stencil of
+    // column t from the dates tile, Lambda~_t = lambda_t c_{t,0}^2, ldl_step_irr)
+    auto factor_row = [&](const IO* t_tt, int k, int t, double w, double lraw, double (&A)[D], double& Dt,
+                          double& idt, double (&mu_t)[D], double& c0) {
+      double vt;
+      if constexpr (IRR) {
+        tile_col<D, IO, NW>(t_tt, k, t, T, mu_t, c0);
+        const double lt = (t < TmD) ? lraw * c0 * c0 : 0.0;
+        ldl_step_irr<D, NW>(S, mu_t, w, lt, 0.0, A, Dt, idt, vt);
+      } else {
+        const double lt = (t < TmD) ? lraw : 0.0;
+        ldl_step<D, NW>(st, w, lt, 0.0, A, Dt, idt, vt);
+      }
+    };
+    // IRR: stencils of the d rows before the chunk (the band warps' recurrences reach back to them)
+    auto publish_pre_mu = [&](double* FMU) {
+      if constexpr (IRR) {
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) FMU[((D - 1 - i) * D + j) * 32] = S.mu[i][j];
+      }
+    };
     // ---- up sweep
     for (int c = 0; c < C; ++c, ++it, ++fb) {
       const int s = it % ST;
@@ -126,6 +158,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       const unsigned char* stg = ring + s * L::F_STAGE;
       const IO* t_w = reinterpret_cast<const IO*>(stg + L::F_OFF_W) + lane;
       const IO* t_lam = reinterpret_cast<const IO*>(stg + L::F_OFF_LAM) + lane;
+      const IO* t_tt = reinterpret_cast<const IO*>(stg + L::F_OFF_TT) + lane;
       const int t0 = c * K;
       if (valid) {
         double* ck = p.ck_fac + (long long)c * NFAC * B + b;
@@ -140,18 +173,23 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       mbar_wait(&fac_empty[fb % L::NFB], (uint32_t)(((fb / L::NFB) & 1) ^ 1));
       unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
       double* FA = reinterpret_cast<double*>(F + L::FB_A) + lane;
+      double* FMU = reinterpret_cast<double*>(F + L::FB_MU) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
+      publish_pre_mu(FMU);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int t = t0 + k;
         const IO wio = t_w[k * 32];
         const double w = to_f64<IO>(wio);
-        double lt = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
-        if (!PD) lt = (t < TmD) ? lt : 0.0;
-        double A[D], Dt, idt, vt;
-        ldl_step<D, NW>(st, w, lt, 0.0, A, Dt, idt, vt);
+        const double lraw = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
+        double A[D], Dt, idt, mu_t[D], c0;
+        factor_row(t_tt, k, t, w, lraw, A, Dt, idt, mu_t, c0);
 #pragma unroll
         for (int j = 0; j < D; ++j) FA[(k * D + j) * 32] = A[j];
+        if constexpr (IRR) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) FMU[((k + D) * D + j) * 32] = mu_t[j];
+        }
         FW[k * 32] = wio;
         if (!BWD && t < T) {
           nobs += (wio > IO(0));
@@ -198,12 +236,21 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       const unsigned char* stg = ring + s * L::F_STAGE;
       const IO* t_w = reinterpret_cast<const IO*>(stg + L::F_OFF_W) + lane;
       const IO* t_lam = reinterpret_cast<const IO*>(stg + L::F_OFF_LAM) + lane;  // row k <-> t0 - D + k
+      const IO* t_tt = reinterpret_cast<const IO*>(stg + L::F_OFF_TT) + lane;
       const int t0 = c * K;
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         const int tj = t0 - 1 - i;
         st.v[i] = 0.0;
-        const double l = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : ((tj >= 0 && tj < TmD) ? lam_s : 0.0);
+        const double lraw = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : lam_s;
+        double l;
+        if constexpr (IRR) {
+          double c0;
+          tile_col<D, IO, NW>(t_tt, -1 - i, tj, T, S.mu[i], c0);
+          l = (tj >= 0 && tj < TmD) ? lraw * c0 * c0 : 0.0;
+        } else {
+          l = PD ? lraw : ((tj >= 0 && tj < TmD) ? lam_s : 0.0);
+        }
         st.lm[i] = l;
         st.id[i] = (tj < 0) ? 1.0 : rcp64<NW>(l + st.dl[i]);
       }
@@ -211,20 +258,27 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
       double* FA = reinterpret_cast<double*>(F + L::FB_A) + lane;
       double* FI = reinterpret_cast<double*>(F + L::FB_ID) + lane;
+      double* FMU = reinterpret_cast<double*>(F + L::FB_MU) + lane;
+      double* FC0 = reinterpret_cast<double*>(F + L::FB_C0) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
+      publish_pre_mu(FMU);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int t = t0 + k;
         const IO wio = t_w[k * 32];
         const double w = to_f64<IO>(wio);
-        double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
-        if (!PD) lt = (t < TmD) ? lt : 0.0;
-        double A[D], Dt, idt, vt;
-        ldl_step<D, NW>(st, w, lt, 0.0, A, Dt, idt, vt);
+        const double lraw = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
+        double A[D], Dt, idt, mu_t[D], c0;
+        factor_row(t_tt, k, t, w, lraw, A, Dt, idt, mu_t, c0);
         const bool past = t >= T;  // rows past the end: z = 0 (q = 0, A = 0)
 #pragma unroll
         for (int j = 0; j < D; ++j) FA[(k * D + j) * 32] = past ? 0.0 : A[j];
         FI[k * 32] = past ? 0.0 : idt + poison;
+        if constexpr (IRR) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) FMU[((k + D) * D + j) * 32] = mu_t[j];
+          FC0[k * 32] = c0;
+        }
         FW[k * 32] = wio;
       }
       __syncwarp();
@@ -288,6 +342,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     mbar_wait(&fac_full[fb % L::NFB], (uint32_t)((fb / L::NFB) & 1));
     const unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
     const double* FA = reinterpret_cast<const double*>(F + L::FB_A) + lane;
+    const double* FMU = reinterpret_cast<const double*>(F + L::FB_MU) + lane;
     const IO* FW = reinterpret_cast<const IO*>(F + L::FB_W) + lane;
     auto up_rows = [&](auto tail_tag) {
       constexpr bool TAIL = decltype(tail_tag)::value;  // the chunk reaches row T: stop there
@@ -301,8 +356,8 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
         for (int u = 0; u < BPW; ++u) {
           double vv = rhs_times_w<IO, BWD>(t_rhs[(u * K + k) * 32], wio, w);
 #pragma unroll
-          for (int j = D; j >= 1; --j) {
-            vv = fma(-Mj(D, j), v[u][j - 1], vv);
+          for (int j = D; j >= 1; --j) {  // M~[t][t-j] = mu_{t-j}[j] (IRR), else M_j
+            vv = fma(-(IRR ? FMU[((k + D - j) * D + j - 1) * 32] : Mj(D, j)), v[u][j - 1], vv);
             vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
           }
 #pragma unroll
@@ -389,6 +444,8 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     const unsigned char* F = fbuf0 + (fb % L::NFB) * L::FBUF;
     const double* FA = reinterpret_cast<const double*>(F + L::FB_A) + lane;
     const double* FI = reinterpret_cast<const double*>(F + L::FB_ID) + lane;
+    const double* FMU = reinterpret_cast<const double*>(F + L::FB_MU) + lane;
+    const double* FC0 = reinterpret_cast<const double*>(F + L::FB_C0) + lane;
     const IO* FW = reinterpret_cast<const IO*>(F + L::FB_W) + lane;
     double q[BPW][K];
 #pragma unroll
@@ -401,7 +458,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
         double vv = rhs_times_w<IO, BWD>(t_rhs[(u * K + k) * 32], wio, w);
 #pragma unroll
         for (int j = D; j >= 1; --j) {
-          vv = fma(-Mj(D, j), v[u][j - 1], vv);
+          vv = fma(-(IRR ? FMU[((k + D - j) * D + j - 1) * 32] : Mj(D, j)), v[u][j - 1], vv);
           vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
         }
 #pragma unroll
@@ -432,13 +489,21 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
         for (int u = 0; u < BPW; ++u) {
           double z = q[u][k];
 #pragma unroll
-          for (int j = D; j >= 1; --j) {
-            z = fma(-Mj(D, j), zw[u][j - 1], z);
+          for (int j = D; j >= 1; --j) {  // M~[t+j][t] = mu_t[j] (IRR), else M_j
+            z = fma(-(IRR ? FMU[((k + D) * D + j - 1) * 32] : Mj(D, j)), zw[u][j - 1], z);
             z = fma(-a[j - 1], zw[u][j - 1], z);
           }
-          double dz = Cj(D, 0) * z;
+          double dz;
+          if constexpr (IRR) {  // (D z)_t = c_{t,0} (z_t + sum_j mu_t[j] z_{t+j})
+            double du = z;
 #pragma unroll
-          for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[u][j - 1], dz);
+            for (int j = 1; j <= D; ++j) du = fma(FMU[((k + D) * D + j - 1) * 32], zw[u][j - 1], du);
+            dz = FC0[k * 32] * du;
+          } else {
+            dz = Cj(D, 0) * z;
+#pragma unroll
+            for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[u][j - 1], dz);
+          }
 #pragma unroll
           for (int i = D - 1; i >= 1; --i) zw[u][i] = zw[u][i - 1];
           zw[u][0] = z;
@@ -449,7 +514,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
             if (ok && in_t) *o0[u] = from_f64<IO>(z);
             if (ok && in_dz) *o1[u] = from_f64<IO>(dz);
           } else {
-            if (sizeof(IO) == 4 && PD) {
+            if (sizeof(IO) == 4 && PD && !IRR) {  // (as the single-series kernels of each grid)
               if (ok && in_t) *o0[u] = wio * from_f64<IO>(z);
               if (u == 0 || two) ls += to_f64<IO>(-(from_f64<IO>(dz) * dzv[u][k]));
             } else {

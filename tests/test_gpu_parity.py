@@ -734,3 +734,54 @@ def test_grad_w_bands_and_autograd():
     P.whit_grad_w(ws1, yp, z1, gy1, gw1)
     torch.cuda.synchronize()
     assert torch.equal(wr.grad, gw1[:, :37])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d,C", [(2, 10), (1, 3), (3, 4)])
+def test_irregular_bands_vs_oracle_and_single_band(d, C, per_date, dtype):
+    """NEXT-1 x NEXT-2 (the paper's Table 1 workload: C bands on uneven dates): whit_forward_times_bands +
+    whit_backward vs the oracle's dense definition per band (dL/dlambda summed over bands), and every
+    band's z and grad_y bitwise equal to the single-band irregular path on that band."""
+    import paper_2604_00048_b200 as P
+
+    T, B = 150, 96
+    lm = "per_date" if per_date else "scalar"
+    x = synth.make_inputs_bands("toy", C, B=B, T=T, d=d, lam_mode=lm, device="cuda", dtype=dtype, seed=70 + d)
+    tt = synth.make_times(B, T, device="cuda", dtype=dtype)
+    y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
+    ws = P.Workspace(d, T, B, dtype, per_date, C=C, times=True)
+    z, gy, gl = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam)
+    P.whit_forward_times_bands(y, w, lam, tt, d, T, B, C, z, ws)
+    P.whit_backward_bands(g, ws, z, gy, gl)
+    assert P.whit_failures(ws) == 0
+    # bitwise: each band through the single-band irregular kernels
+    ws1 = P.Workspace(d, T, B, dtype, per_date, times=True)
+    for c in range(C):
+        z1, gy1, gl1 = torch.empty_like(y[c]), torch.empty_like(y[c]), torch.empty_like(lam)
+        P.whit_forward_times(y[c].contiguous(), w, lam, tt, d, T, B, z1, ws1)
+        P.whit_backward(g[c].contiguous(), ws1, z1, gy1, gl1)
+        assert torch.equal(z[c], z1), c
+        assert torch.equal(gy[c], gy1), c
+    torch.cuda.synchronize()
+    tz, tg = TOL[(dtype, d)]
+    if d == 3 and dtype == torch.float32:
+        tz, tg = 1e-3, 1e-2
+    th = tt.double().cpu().numpy().T
+    wn = w.double().cpu().numpy().T
+    ln = lam.double().cpu().numpy()
+    ln = ln.T if ln.ndim == 2 else ln
+    for b in (0, 37, 95):
+        o = [O1.forward_backward_times(y[c, :, b].double().cpu().numpy(), wn[b], ln[b], th[b], d,
+                                       g[c, :, b].double().cpu().numpy()) for c in range(C)]
+        for c in range(C):
+            ez = np.max(np.abs(z[c, :, b].double().cpu().numpy() - o[c]["z"].astype(float)))
+            assert ez / ymax_observed(y[c, :, b].double().cpu().numpy(), wn[b]) <= tz, (b, c, ez)
+            assert rel_series(gy[c, :, b].double().cpu().numpy(), o[c]["ybar"]).max() <= tg, (b, c)
+        ref = sum(oc["lambar"] for oc in o)
+        if per_date:
+            assert rel_series(gl[:, b].double().cpu().numpy(), ref).max() <= tg, b
+        else:
+            Dm = O1.difference_matrix_times(th[b], d)
+            den = sum(np.sum(np.abs((-(Dm @ oc["u"]) * oc["dz"]).astype(float))) for oc in o)
+            assert abs(gl[b].item() - float(ref)) / den <= tg, b
