@@ -32,6 +32,10 @@ struct MB2Layout {
 #endif
   // rows per chunk; TMA ring slots (ST - 1 chunks of loads in flight per warp); bands per band warp
   static constexpr int K = WHIT_MB2_K, ST = WHIT_MB2_ST, BPW = 2;
+  // factor-warp ring slots: the factor warp's per-chunk work is short (K rows of the recurrence), so
+  // in the forward its w / lambda (/ dates) loads are issued 3 chunks ahead to cover the HBM latency
+  // (measured: forward faster, backward not -- its smem goes to the reduction rows)
+  static constexpr int FST = BWD ? 2 : 4;
   static constexpr int ROW = 32 * (int)sizeof(IO);
   // factor warp ring: w K rows | lambda K (+d) rows | IRR: acquisition dates K+2d rows (t0-d .. t0+K+d-1)
   static constexpr int F_OFF_W = 0, F_OFF_LAM = K * ROW;
@@ -50,9 +54,9 @@ struct MB2Layout {
   static constexpr uint32_t F_BYTES_UP = (K + (PD ? K : 0) + (IRR ? K + 2 * D : 0)) * ROW;
   static constexpr uint32_t F_BYTES_DN = (K + (PD ? K + D : 0) + (IRR ? K + 2 * D : 0)) * ROW;
   // smem: factor ring | factor buffers | band warps | per-warp reduction rows (fp64) + scalars
-  static constexpr int OFF_FB = ST * F_STAGE;
+  static constexpr int OFF_FB = FST * F_STAGE;
   // factor buffers in flight: enough that the factor warp runs ahead of the band warps' jitter
-  static constexpr int NFB = (BWD && PD) ? 3 : 4;
+  static constexpr int NFB = (BWD && !PD) ? 4 : 3;
   static constexpr int OFF_BAND = OFF_FB + NFB * FBUF;
   __host__ __device__ static constexpr int nwarps(int nb) { return (nb + BPW - 1) / BPW; }
   static constexpr int smem(int nb) {
@@ -67,9 +71,9 @@ struct MB2Layout {
 template <int D, typename IO, bool PD, bool BWD, bool IRR = false>
 __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_constant__ Params p) {
   using L = MB2Layout<D, IO, PD, BWD, IRR>;
-  constexpr int K = L::K, ST = L::ST, NFAC = Ck<D>::NFAC, NW = Newton<IO>::N, BPW = L::BPW;
+  constexpr int K = L::K, ST = L::ST, FST = L::FST, NFAC = Ck<D>::NFAC, NW = Newton<IO>::N, BPW = L::BPW;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t f_full[ST];
+  __shared__ __align__(8) uint64_t f_full[FST];
   __shared__ __align__(8) uint64_t b_full[(kMaxBands + 1) / 2][ST];
   __shared__ __align__(8) uint64_t fac_full[L::NFB], fac_empty[L::NFB];
 
@@ -92,7 +96,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
   }
   if (lane == 0) {
     if (fwarp) {
-      for (int s = 0; s < ST; ++s) mbar_init(&f_full[s], 1);
+      for (int s = 0; s < FST; ++s) mbar_init(&f_full[s], 1);
     } else {
       for (int s = 0; s < ST; ++s) mbar_init(&b_full[warp][s], 1);
     }
@@ -107,17 +111,17 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       const bool up = i < C;
       const int c = up ? i : 2 * C - 1 - i;
       const int t0 = c * K;
-      unsigned char* stg = ring + (i % ST) * L::F_STAGE;
-      mbar_arrive_expect_tx(&f_full[i % ST], up ? L::F_BYTES_UP : L::F_BYTES_DN);
-      tma_load_2d(stg + L::F_OFF_W, &p.tm_w, (int)bw, t0, &f_full[i % ST]);
+      unsigned char* stg = ring + (i % FST) * L::F_STAGE;
+      mbar_arrive_expect_tx(&f_full[i % FST], up ? L::F_BYTES_UP : L::F_BYTES_DN);
+      tma_load_2d(stg + L::F_OFF_W, &p.tm_w, (int)bw, t0, &f_full[i % FST]);
       if (PD) {
-        if (up) tma_load_2d(stg + L::F_OFF_LAM, &p.tm_lam_up, (int)bw, t0, &f_full[i % ST]);
-        else tma_load_2d(stg + L::F_OFF_LAM, &p.tm_lam_dn, (int)bw, t0 - D, &f_full[i % ST]);
+        if (up) tma_load_2d(stg + L::F_OFF_LAM, &p.tm_lam_up, (int)bw, t0, &f_full[i % FST]);
+        else tma_load_2d(stg + L::F_OFF_LAM, &p.tm_lam_dn, (int)bw, t0 - D, &f_full[i % FST]);
       }
-      if (IRR) tma_load_2d(stg + L::F_OFF_TT, &p.tm_lw, (int)bw, t0 - D, &f_full[i % ST]);  // dates
+      if (IRR) tma_load_2d(stg + L::F_OFF_TT, &p.tm_lw, (int)bw, t0 - D, &f_full[i % FST]);  // dates
     };
     if (lane == 0)
-      for (int i = 0; i < ST && i < ntiles; ++i) issue(i);
+      for (int i = 0; i < FST && i < ntiles; ++i) issue(i);
     __syncwarp();
     const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
     IState<D> S;  // factor recurrence state (S.mu: stencils of the last d columns, IRR only)
@@ -153,8 +157,8 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     };
     // ---- up sweep
     for (int c = 0; c < C; ++c, ++it, ++fb) {
-      const int s = it % ST;
-      mbar_wait(&f_full[s], (uint32_t)((it / ST) & 1));
+      const int s = it % FST;
+      mbar_wait(&f_full[s], (uint32_t)((it / FST) & 1));
       const unsigned char* stg = ring + s * L::F_STAGE;
       const IO* t_w = reinterpret_cast<const IO*>(stg + L::F_OFF_W) + lane;
       const IO* t_lam = reinterpret_cast<const IO*>(stg + L::F_OFF_LAM) + lane;
@@ -198,9 +202,9 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&fac_full[fb % L::NFB]);  // release: this warp's smem writes
-      if (lane == 0 && it + ST < ntiles) {
+      if (lane == 0 && it + FST < ntiles) {
         fence_proxy_async_smem();
-        issue(it + ST);
+        issue(it + FST);
       }
     }
     bool failed;
@@ -221,7 +225,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     };
     load_ck(C - 1);
     for (int c = C - 1; c >= 0; --c, ++it, ++fb) {
-      const int s = it % ST;
+      const int s = it % FST;
       {
         int f = 0;
 #pragma unroll
@@ -232,7 +236,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
           for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = ckn[f++];
       }
       if (c > 0) load_ck(c - 1);
-      mbar_wait(&f_full[s], (uint32_t)((it / ST) & 1));
+      mbar_wait(&f_full[s], (uint32_t)((it / FST) & 1));
       const unsigned char* stg = ring + s * L::F_STAGE;
       const IO* t_w = reinterpret_cast<const IO*>(stg + L::F_OFF_W) + lane;
       const IO* t_lam = reinterpret_cast<const IO*>(stg + L::F_OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -283,9 +287,9 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&fac_full[fb % L::NFB]);
-      if (lane == 0 && it + ST < ntiles) {
+      if (lane == 0 && it + FST < ntiles) {
         fence_proxy_async_smem();
-        issue(it + ST);
+        issue(it + FST);
       }
     }
     if (BWD && !PD) __syncthreads();  // matches the band warps' scalar-lambda reduction
