@@ -425,12 +425,17 @@ def run_libwhit(args):
                                    "algorithmic_bytes": dbytes, "fwd_ms": round(fa, 4), "bwd_ms": round(ba, 4)}}
         del bits
 
-    # end to end through the public API with host buffers (rank-local)
+    # end to end through the public API with host buffers (rank-local); also with the binary W shipped
+    # as bits (whit_run_host_wbits), reported beside it
     e2e = None
+    e2e_wbits = None
     if not args.no_e2e:
+        bits_h = P.whit_pack_mask(w).cpu() if args.config == "hetero" else None
         del wsp, z, gy, gl
         torch.cuda.empty_cache()
         e2e = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps)
+        if bits_h is not None:
+            e2e_wbits = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, wbits=bits_h)
 
     # CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
@@ -456,7 +461,7 @@ def run_libwhit(args):
                        "mask": "Sentinel-2 revisit + seasonal clouds, 90-day trailing gap",
                        "failed_series": nfail},
             "roofline": roof, "gpu_launches": 2 * K, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
-            "w_bits": wbits_line, "checksums": checksums,
+            "w_bits": wbits_line, "e2e_wbits": e2e_wbits, "checksums": checksums,
         }
         print(json.dumps(line), flush=True)
     if distributed:
@@ -642,20 +647,27 @@ def run_s2tile(args, P, synth, dev, ws_n, rank):
     return 0
 
 
-def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6):
+def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6, wbits=None):
     """Same metric through the public C-ABI with pinned HOST buffers: whit_run_host streams the
     batch in series chunks (pitched 2-D H2D copies of y, w, lambda, g; whit_forward +
-    whit_backward; D2H of z, grad_y, grad_lambda), copies overlapping kernels on nbuf streams."""
+    whit_backward; D2H of z, grad_y, grad_lambda), copies overlapping kernels on nbuf streams.
+    With ``wbits`` (host bit-packed W) the weights cross PCIe as bits (whit_run_host_wbits)."""
     import torch
-    h = {k: torch.empty(x[k].shape, dtype=io, pin_memory=True) for k in ("y", "w", "lam", "g")}
+    keys = ("y", "lam", "g") if wbits is not None else ("y", "w", "lam", "g")
+    h = {k: torch.empty(x[k].shape, dtype=io, pin_memory=True) for k in keys}
     for k in h:
         h[k].copy_(x[k])
+    if wbits is not None:
+        h["wbits"] = wbits.pin_memory()
     oz = torch.empty(x["y"].shape, dtype=io, pin_memory=True)
     oy = torch.empty(x["y"].shape, dtype=io, pin_memory=True)
     ol = torch.empty(x["lam"].shape, dtype=io, pin_memory=True)
     h2d = sum(t.numel() * t.element_size() for t in h.values())
     d2h = sum(t.numel() * t.element_size() for t in (oz, oy, ol))
-    buf = P.whit_run_host(h["y"], h["w"], h["lam"], h["g"], d, oz, oy, ol, chunk=chunk, nbuf=nbuf, stream=stream)
+    hw = h.get("w", h["y"])
+    bits = h.get("wbits")
+    buf = P.whit_run_host(h["y"], hw, h["lam"], h["g"], d, oz, oy, ol, chunk=chunk, nbuf=nbuf, stream=stream,
+                          wbits=bits)
     torch.cuda.synchronize(dev)
     ws_n = int(os.environ.get("WORLD_SIZE", "1"))
     import torch.distributed as dist
@@ -664,14 +676,15 @@ def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
-        P.whit_run_host(h["y"], h["w"], h["lam"], h["g"], d, oz, oy, ol, chunk=chunk, nbuf=nbuf, dev_buf=buf,
-                        stream=stream)
+        P.whit_run_host(h["y"], hw, h["lam"], h["g"], d, oz, oy, ol, chunk=chunk, nbuf=nbuf, dev_buf=buf,
+                        stream=stream, wbits=bits)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(e0.elapsed_time(e1) / steps, dev)
     return {"value": ws_n * B / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": ms, "steps": steps, "api": f"whit_run_host (C-ABI, pinned host buffers, chunk {chunk}, "
-                                                       f"{nbuf} streams)"}
+            "ms_per_step": ms, "steps": steps,
+            "api": f"{'whit_run_host_wbits' if bits is not None else 'whit_run_host'} (C-ABI, pinned host buffers, "
+                   f"chunk {chunk}, {nbuf} streams)"}
 
 
 def main():

@@ -317,6 +317,15 @@ whit_status whit_run_host(const void* y, const void* w, const void* lambda, cons
                           void* grad_lambda, int32_t* info, int64_t chunk, int nbuf, void* dev_buf,
                           size_t dev_bytes, void* cuda_stream);
 
+/* The same with the binary W as bits (HOST uint32 [ceil(T/32)][B], the layout
+ * of whit_pack_mask): 1/32 of the weight plane's PCIe bytes; each chunk runs
+ * whit_forward_wbits (+ whit_backward).  Results equal whit_run_host with the
+ * 0/1 float plane bit for bit.  Same device scratch size. */
+whit_status whit_run_host_wbits(const void* y, const uint32_t* wbits, const void* lambda, const void* grad_z, int d,
+                                int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode, void* z,
+                                void* grad_y, void* grad_lambda, int32_t* info, int64_t chunk, int nbuf,
+                                void* dev_buf, size_t dev_bytes, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

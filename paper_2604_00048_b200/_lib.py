@@ -60,6 +60,8 @@ SIGNATURES = [
     ("whit_host_ws_bytes", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("whit_run_host", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                      _VP, _VP, _VP, _VP, _I64, ctypes.c_int, _VP, _SZ, _VP]),
+    ("whit_run_host_wbits", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
+                                           _VP, _VP, _VP, _VP, _I64, ctypes.c_int, _VP, _SZ, _VP]),
 ]
 
 
@@ -227,21 +229,24 @@ def whit_host_ws_bytes(d: int, T: int, chunk: int, dtype, per_date: bool, nbuf: 
 
 
 def whit_run_host(y, w, lam, grad_z, d: int, z, grad_y=None, grad_lambda=None, info=None, *, chunk: int = 16384,
-                  nbuf: int = 3, dev_buf=None, stream=None):
+                  nbuf: int = 3, dev_buf=None, stream=None, wbits=None):
     """Streaming executor over HOST (CPU, ideally pinned) tensors in [T][B] layout.
 
     ``dev_buf`` (uint8 CUDA tensor of >= whit_host_ws_bytes bytes) is allocated if not given.
-    Returns the device buffer (reuse it across calls).  Asynchronous on ``stream``.
+    Returns the device buffer (reuse it across calls).  Asynchronous on ``stream``.  With ``wbits`` (HOST
+    int32/uint32 [ceil(T/32)][B], the bit-packed binary W) ``w`` is ignored and whit_run_host_wbits runs.
     """
     T, B = y.shape
     per_date = lam.dim() == 2
     need = whit_host_ws_bytes(d, T, min(chunk, B), y.dtype, per_date, nbuf)
     if dev_buf is None or dev_buf.numel() < need:
         dev_buf = torch.empty(need, dtype=torch.uint8, device="cuda")
-    for t in (y, w, lam, z) + ((grad_z, grad_y, grad_lambda) if grad_z is not None else ()):
+    wt = wbits if wbits is not None else w
+    for t in (y, wt, lam, z) + ((grad_z, grad_y, grad_lambda) if grad_z is not None else ()):
         if t.is_cuda or not t.is_contiguous():
             raise ValueError("whit_run_host takes contiguous HOST tensors")
-    _check(_lib.whit_run_host(_ptr(y), _ptr(w), _ptr(lam), _ptr(grad_z), d, T, B, _dtype_code(y.dtype), int(per_date),
+    fn = _lib.whit_run_host_wbits if wbits is not None else _lib.whit_run_host
+    _check(fn(_ptr(y), _ptr(wt), _ptr(lam), _ptr(grad_z), d, T, B, _dtype_code(y.dtype), int(per_date),
                               _ptr(z), _ptr(grad_y), _ptr(grad_lambda), _ptr(info), min(chunk, B), nbuf,
                               ctypes.c_void_p(dev_buf.data_ptr()), dev_buf.numel(), _stream_handle(stream)),
            "whit_run_host")

@@ -61,11 +61,16 @@ size_t whit_host_ws_bytes(int d, int64_t T, int64_t chunk, whit_dtype dtype, whi
   return size_t(nbuf) * L.total;
 }
 
-whit_status whit_run_host(const void* y, const void* w, const void* lambda, const void* grad_z, int d, int64_t T,
-                          int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode, void* z, void* grad_y,
-                          void* grad_lambda, int32_t* info, int64_t chunk, int nbuf, void* dev_buf,
-                          size_t dev_bytes, void* cuda_stream) {
-  if (!y || !w || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL host pointer");
+}  // extern "C"
+
+namespace {
+
+// w (a [T][B] weight plane) or wbits (the bit-packed binary W, [ceil(T/32)][B] uint32) -- exactly one.
+whit_status run_host(const void* y, const void* w, const uint32_t* wbits, const void* lambda, const void* grad_z,
+                     int d, int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode, void* z,
+                     void* grad_y, void* grad_lambda, int32_t* info, int64_t chunk, int nbuf, void* dev_buf,
+                     size_t dev_bytes, void* cuda_stream) {
+  if (!y || !(w || wbits) || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL host pointer");
   if (grad_z && (!grad_y || !grad_lambda)) return fail(WHIT_ERR_ARG, "grad_z given without grad_y / grad_lambda");
   if (dtype != WHIT_F32 && dtype != WHIT_F64) return fail(WHIT_ERR_ARG, "bad dtype");
   if (lambda_mode != WHIT_LAMBDA_SCALAR && lambda_mode != WHIT_LAMBDA_PER_DATE) return fail(WHIT_ERR_ARG, "bad lambda mode");
@@ -117,14 +122,21 @@ whit_status whit_run_host(const void* y, const void* w, const void* lambda, cons
                               cudaMemcpyDeviceToHost, st[s]);
     };
     h2d(L.y, y, T);
-    h2d(L.w, w, T);
+    if (w) {
+      h2d(L.w, w, T);
+    } else if (e == cudaSuccess) {  // bits: ceil(T/32) rows of bc uint32 words
+      e = cudaMemcpy2DAsync(sb + L.w, size_t(bc) * 4, reinterpret_cast<const char*>(wbits) + size_t(b0) * 4,
+                            size_t(B) * 4, size_t(bc) * 4, size_t((T + 31) / 32), cudaMemcpyHostToDevice, st[s]);
+    }
     h2d(L.lam, lambda, TL);
     if (grad_z) h2d(L.g, grad_z, T);
     if (e != cudaSuccess) break;
     whit_ws* ws = nullptr;
     status = whit_ws_create(&ws, d, T, bc, dtype, lambda_mode, sb + L.ws, L.total - L.ws, st[s]);
     if (status != WHIT_OK) break;
-    status = whit_forward(sb + L.y, sb + L.w, sb + L.lam, d, T, bc, sb + L.z, ws);
+    status = w ? whit_forward(sb + L.y, sb + L.w, sb + L.lam, d, T, bc, sb + L.z, ws)
+               : whit_forward_wbits(sb + L.y, reinterpret_cast<const uint32_t*>(sb + L.w), sb + L.lam, d, T, bc,
+                                    sb + L.z, ws);
     if (status == WHIT_OK && grad_z) status = whit_backward(sb + L.g, ws, sb + L.z, sb + L.gy, sb + L.gl);
     const int32_t* dinfo = whit_info_device(ws);
     whit_ws_destroy(ws);  // host handle only; the enqueued work does not reference it
@@ -152,6 +164,28 @@ whit_status whit_run_host(const void* y, const void* w, const void* lambda, cons
   if (status != WHIT_OK) return status;
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "whit_run_host: %s", cudaGetErrorString(e));
   return WHIT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+whit_status whit_run_host(const void* y, const void* w, const void* lambda, const void* grad_z, int d, int64_t T,
+                          int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode, void* z, void* grad_y,
+                          void* grad_lambda, int32_t* info, int64_t chunk, int nbuf, void* dev_buf,
+                          size_t dev_bytes, void* cuda_stream) {
+  if (!w) return fail(WHIT_ERR_ARG, "NULL host pointer");
+  return run_host(y, w, nullptr, lambda, grad_z, d, T, B, dtype, lambda_mode, z, grad_y, grad_lambda, info, chunk,
+                  nbuf, dev_buf, dev_bytes, cuda_stream);
+}
+
+whit_status whit_run_host_wbits(const void* y, const uint32_t* wbits, const void* lambda, const void* grad_z, int d,
+                                int64_t T, int64_t B, whit_dtype dtype, whit_lambda_mode lambda_mode, void* z,
+                                void* grad_y, void* grad_lambda, int32_t* info, int64_t chunk, int nbuf,
+                                void* dev_buf, size_t dev_bytes, void* cuda_stream) {
+  if (!wbits) return fail(WHIT_ERR_ARG, "NULL host pointer");
+  return run_host(y, nullptr, wbits, lambda, grad_z, d, T, B, dtype, lambda_mode, z, grad_y, grad_lambda, info,
+                  chunk, nbuf, dev_buf, dev_bytes, cuda_stream);
 }
 
 }  // extern "C"

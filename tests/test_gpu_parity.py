@@ -246,6 +246,32 @@ def test_host_executor_matches_device_path_bitwise(dtype, per_date):
     assert np.array_equal(info.numpy(), dev["info"])
 
 
+@pytest.mark.parametrize("per_date", [True, False])
+def test_host_executor_wbits_equals_float_w(per_date):
+    """whit_run_host_wbits (HOST bit-packed W) returns exactly whit_run_host's results with the 0/1 plane."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 300, 1000
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, lam_mode="per_date" if per_date else "scalar",
+                          device="cuda", seed=79)
+    bits = P.whit_pack_mask(x["w"])
+    torch.cuda.synchronize()
+    h = {k: x[k].cpu().pin_memory() for k in ("y", "w", "lam", "g")}
+    hb = bits.cpu().pin_memory()
+    outs = []
+    for use_bits in (False, True):
+        z = torch.empty_like(h["y"]).pin_memory()
+        gy = torch.empty_like(h["y"]).pin_memory()
+        gl = torch.empty_like(h["lam"]).pin_memory()
+        info = torch.empty(B, dtype=torch.int32).pin_memory()
+        P.whit_run_host(h["y"], h["w"], h["lam"], h["g"], d, z, gy, gl, info, chunk=256, nbuf=3,
+                        wbits=hb if use_bits else None)
+        torch.cuda.synchronize()
+        outs.append((z, gy, gl, info))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("chunk,nbuf", [(4096, 2), (96, 5)])
 def test_host_executor_forward_only_and_chunking(chunk, nbuf):
     """whit_run_host without grad_z (forward only; info still reported), with one chunk larger than B
