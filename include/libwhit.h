@@ -179,9 +179,10 @@ whit_status whit_grad_w(whit_ws* factor_ws, const void* y, const void* z, const 
  * the band warps through shared memory (two bands per band warp), so w,
  * lambda and factor-checkpoint bytes and the factor's fp64 work are amortised
  * over C bands; every band's z and grad_y equal the single-band results bit
- * for bit.  The single-band entry points above are the C = 1 case
- * (whit_forward on a C > 1 workspace is WHIT_ERR_SHAPE; whit_backward works
- * for any C). */
+ * for bit.  info (one per pixel): T-d+1 (< d observed days), -1 (another
+ * non-positive pivot; the single-band kernels report its exact row).  The
+ * single-band entry points above are the C = 1 case (whit_forward on a C > 1
+ * workspace is WHIT_ERR_SHAPE; whit_backward works for any C). */
 size_t whit_ws_bytes_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype, whit_lambda_mode lambda_mode);
 
 whit_status whit_ws_create_bands(whit_ws** out, int d, int64_t T, int64_t B, int C, whit_dtype dtype,
