@@ -158,20 +158,42 @@ class Workspace:
             self.handle = None
 
 
+def _shapes(ws: "Workspace", where: str, lam, *planes, C: int = 1):
+    """Tensor-shape checks the pointer ABI cannot make: lambda's mode must match the workspace
+    ((T-d, B) per date, (B,) scalar) and the [T][B] / [C][T][B] planes must have the workspace's shape."""
+    T, B, d = ws.T, ws.B, ws.d
+    want = (T - d, B) if ws.per_date else (B,)
+    if tuple(lam.shape) != want:
+        raise ValueError(f"{where}: lambda shape {tuple(lam.shape)} != {want} "
+                         f"({'per-date' if ws.per_date else 'scalar'} workspace)")
+    for name, t, shp in planes:
+        exp = {"TB": (T, B), "CTB": (C, T, B) if C > 1 else None}[shp]
+        if exp is None:
+            ok = tuple(t.shape) in ((T, B), (1, T, B))
+        else:
+            ok = tuple(t.shape) == exp
+        if not ok:
+            raise ValueError(f"{where}: {name} shape {tuple(t.shape)} does not match the workspace (T={T}, B={B}, C={C})")
+
+
 def whit_forward(y, w, lam, d: int, T: int, B: int, z, ws: Workspace):
+    _shapes(ws, "whit_forward", lam, ("y", y, "TB"), ("w", w, "TB"), ("z", z, "TB"))
     _check(_lib.whit_forward(_ptr(y), _ptr(w), _ptr(lam), d, T, B, _ptr(z), ws.handle), "whit_forward")
 
 
 def whit_forward_bands(y, w, lam, d: int, T: int, B: int, C: int, z, ws: Workspace):
+    _shapes(ws, "whit_forward_bands", lam, ("y", y, "CTB"), ("w", w, "TB"), ("z", z, "CTB"), C=C)
     _check(_lib.whit_forward_bands(_ptr(y), _ptr(w), _ptr(lam), d, T, B, C, _ptr(z), ws.handle), "whit_forward_bands")
 
 
 def whit_backward_bands(grad_z, ws: Workspace, z, grad_y, grad_lambda):
+    _shapes(ws, "whit_backward_bands", grad_lambda, ("grad_z", grad_z, "CTB"), ("grad_y", grad_y, "CTB"), C=ws.C)
     _check(_lib.whit_backward_bands(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)),
            "whit_backward_bands")
 
 
 def whit_backward(grad_z, ws: Workspace, z, grad_y, grad_lambda):
+    _shapes(ws, "whit_backward", grad_lambda, ("grad_z", grad_z, "CTB"), ("grad_y", grad_y, "CTB"), C=ws.C)
     _check(_lib.whit_backward(_ptr(grad_z), ws.handle, _ptr(z), _ptr(grad_y), _ptr(grad_lambda)), "whit_backward")
 
 
@@ -181,12 +203,15 @@ def whit_grad_w(ws: Workspace, y, z, grad_y, grad_w):
 
 
 def whit_forward_times(y, w, lam, times, d: int, T: int, B: int, z, ws: Workspace):
+    _shapes(ws, "whit_forward_times", lam, ("y", y, "TB"), ("w", w, "TB"), ("times", times, "TB"), ("z", z, "TB"))
     _check(_lib.whit_forward_times(_ptr(y), _ptr(w), _ptr(lam), _ptr(times), d, T, B, _ptr(z), ws.handle),
            "whit_forward_times")
 
 
 def whit_forward_times_bands(y, w, lam, times, d: int, T: int, B: int, C: int, z, ws: Workspace):
     """C bands per pixel on uneven dates (y, z: [C][T][B]; w, lam, times shared)."""
+    _shapes(ws, "whit_forward_times_bands", lam, ("y", y, "CTB"), ("w", w, "TB"), ("times", times, "TB"),
+            ("z", z, "CTB"), C=C)
     _check(_lib.whit_forward_times_bands(_ptr(y), _ptr(w), _ptr(lam), _ptr(times), d, T, B, C, _ptr(z), ws.handle),
            "whit_forward_times_bands")
 
@@ -201,15 +226,19 @@ def whit_pack_mask(w, bits=None, stream=None):
 
 
 def whit_forward_wbits(y, wbits, lam, d: int, T: int, B: int, z, ws: Workspace):
+    _shapes(ws, "whit_forward_wbits", lam, ("y", y, "TB"), ("z", z, "TB"))
     _check(_lib.whit_forward_wbits(_ptr(y), _ptr(wbits), _ptr(lam), d, T, B, _ptr(z), ws.handle), "whit_forward_wbits")
 
 
 def whit_forward_mse(y, w, lam, loss_w, d: int, T: int, B: int, z, grad_z, loss, ws: Workspace):
+    _shapes(ws, "whit_forward_mse", lam, ("y", y, "TB"), ("w", w, "TB"), ("loss_w", loss_w, "TB"), ("z", z, "TB"),
+            ("grad_z", grad_z, "TB"))
     _check(_lib.whit_forward_mse(_ptr(y), _ptr(w), _ptr(lam), _ptr(loss_w), d, T, B, _ptr(z), _ptr(grad_z), _ptr(loss),
                                  ws.handle), "whit_forward_mse")
 
 
 def whit_posterior_variance(w, lam, d: int, T: int, B: int, var, ws: Workspace):
+    _shapes(ws, "whit_posterior_variance", lam, ("w", w, "TB"), ("var", var, "TB"))
     _check(_lib.whit_posterior_variance(_ptr(w), _ptr(lam), d, T, B, _ptr(var), ws.handle), "whit_posterior_variance")
 
 

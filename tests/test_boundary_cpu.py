@@ -108,3 +108,25 @@ def test_python_binding_refuses_cpu_tensors():
     y = torch.zeros(10, 4)
     with pytest.raises(ValueError):
         P.smooth(y, y, torch.ones(8, 4), 2)
+
+
+def test_python_binding_rejects_mismatched_lambda_mode_and_shapes():
+    """The pointer ABI cannot see tensor shapes; the binding checks lambda's mode and the planes' shapes
+    against the workspace before any launch (host-only: works without a GPU)."""
+    import types
+
+    import pytest
+    import torch
+    from paper_2604_00048_b200 import _lib as L
+
+    ws = types.SimpleNamespace(T=50, B=8, d=2, C=1, per_date=True)
+    y = torch.zeros(50, 8)
+    with pytest.raises(ValueError, match="lambda shape"):
+        L._shapes(ws, "whit_forward", torch.zeros(8), ("y", y, "TB"))
+    with pytest.raises(ValueError, match="y shape"):
+        L._shapes(ws, "whit_forward", torch.zeros(48, 8), ("y", torch.zeros(49, 8), "TB"))
+    L._shapes(ws, "whit_forward", torch.zeros(48, 8), ("y", y, "TB"))
+    ws3 = types.SimpleNamespace(T=50, B=8, d=2, C=3, per_date=False)
+    L._shapes(ws3, "whit_forward_bands", torch.zeros(8), ("y", torch.zeros(3, 50, 8), "CTB"), C=3)
+    with pytest.raises(ValueError):
+        L._shapes(ws3, "whit_forward_bands", torch.zeros(8), ("y", torch.zeros(2, 50, 8), "CTB"), C=3)

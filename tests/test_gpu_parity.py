@@ -811,3 +811,41 @@ def test_irregular_bands_vs_oracle_and_single_band(d, C, per_date, dtype):
             Dm = O1.difference_matrix_times(th[b], d)
             den = sum(np.sum(np.abs((-(Dm @ oc["u"]) * oc["dz"]).astype(float))) for oc in o)
             assert abs(gl[b].item() - float(ref)) / den <= tg, b
+
+
+@pytest.mark.parametrize("times", [False, True])
+def test_bands_degenerate_pixels(times):
+    """Multi-band status: a pixel with fewer than d observed days gets info = T-d+1 and NaN in every band's
+    z, grad_y and in its grad_lambda; its neighbours are unaffected (their results equal a run without it)."""
+    import paper_2604_00048_b200 as P
+
+    d, C, T, B = 2, 3, 120, 64
+    x = synth.make_inputs_bands("toy", C, B=B, T=T, d=d, lam_mode="per_date", device="cuda", seed=90)
+    tt = synth.make_times(B, T, device="cuda") if times else None
+
+    def run(w):
+        ws = P.Workspace(d, T, B, torch.float32, True, C=C, times=times)
+        z, gy, gl = torch.empty_like(x["y"]), torch.empty_like(x["y"]), torch.empty_like(x["lam"])
+        if times:
+            P.whit_forward_times_bands(x["y"], w, x["lam"], tt, d, T, B, C, z, ws)
+        else:
+            P.whit_forward_bands(x["y"], w, x["lam"], d, T, B, C, z, ws)
+        P.whit_backward_bands(x["g"], ws, z, gy, gl)
+        n, info = P.whit_failures(ws, with_info=True)
+        return z, gy, gl, n, info
+
+    w = x["w"].clone()
+    w[:, 5] = 0.0          # no observation
+    w[:, 9] = 0.0
+    w[17, 9] = 1.0         # one observation (< d)
+    z, gy, gl, n, info = run(w)
+    assert n == 2 and info[5] == T - d + 1 and info[9] == T - d + 1
+    for b in (5, 9):
+        assert torch.isnan(z[:, :, b]).all() and torch.isnan(gy[:, :, b]).all() and torch.isnan(gl[:, b]).all()
+    ok = [b for b in range(B) if b not in (5, 9)]
+    w2 = x["w"].clone()
+    w2[:, 5] = 1.0
+    w2[:, 9] = 1.0
+    z2, gy2, gl2, _, _ = run(w2)
+    assert torch.equal(z[:, :, ok], z2[:, :, ok]) and torch.equal(gy[:, :, ok], gy2[:, :, ok])
+    assert torch.equal(gl[:, ok], gl2[:, ok])
