@@ -31,7 +31,10 @@ struct MB2Layout {
 #define WHIT_MB2_ST 2
 #endif
   // rows per chunk; TMA ring slots (ST - 1 chunks of loads in flight per warp); bands per band warp
-  static constexpr int K = WHIT_MB2_K, ST = WHIT_MB2_ST, BPW = 2;
+#ifndef WHIT_MB2_BPW
+#define WHIT_MB2_BPW 2
+#endif
+  static constexpr int K = WHIT_MB2_K, ST = WHIT_MB2_ST, BPW = WHIT_MB2_BPW;
   // factor-warp ring slots: the factor warp's per-chunk work is short (K rows of the recurrence), so
   // in the forward its w / lambda (/ dates) loads are issued 3 chunks ahead to cover the HBM latency
   // (measured: forward faster, backward not -- its smem goes to the reduction rows)
@@ -299,8 +302,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
   // ============================================================== band warps (two bands each)
   const int bj = warp;
   const int cb0 = bj * BPW;
-  const bool two = cb0 + 1 < nb;
-  const bool ok1 = valid && two;  // this warp's second band exists
+  const int nbw = min(BPW, nb - cb0);  // bands of this warp (the last warp may hold fewer)
   unsigned char* ring = smem + L::OFF_BAND + bj * L::B_WARP;
   double* redw0 = reinterpret_cast<double*>(smem + L::OFF_BAND + nw * L::B_WARP);  // [2][nw][K][32] (PD bwd)
   double* redS = redw0 + (BWD && PD ? 2 * nw * K * 32 : 0);                          // [nw][32]
@@ -310,9 +312,8 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     const int c = up ? i : 2 * C - 1 - i;
     const int t0 = c * K;
     unsigned char* stg = ring + (i % ST) * L::B_STAGE;
-    mbar_arrive_expect_tx(&bars[i % ST], (two ? 2 : 1) * K * L::ROW);
-    tma_load_3d(stg, &p.tm_rhs, (int)bw, t0, cb0, &bars[i % ST]);
-    if (two) tma_load_3d(stg + K * L::ROW, &p.tm_rhs, (int)bw, t0, cb0 + 1, &bars[i % ST]);
+    mbar_arrive_expect_tx(&bars[i % ST], nbw * K * L::ROW);
+    for (int u = 0; u < nbw; ++u) tma_load_3d(stg + u * K * L::ROW, &p.tm_rhs, (int)bw, t0, cb0 + u, &bars[i % ST]);
   };
   if (lane == 0)
     for (int i = 0; i < ST && i < ntiles; ++i) issue(i);
@@ -337,7 +338,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     if (valid) {
 #pragma unroll
       for (int u = 0; u < BPW; ++u) {
-        if (u == 1 && !two) break;
+        if (u >= nbw) break;
         double* ck = ck_rhs + (long long)c * ck_stride + (long long)(cb0 + u) * D * B;
 #pragma unroll
         for (int i = 0; i < D; ++i) ck[(long long)i * B] = v[u][i];
@@ -395,7 +396,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
 #pragma unroll
     for (int u = 0; u < BPW; ++u) {
       const double* ck = ck_rhs + (long long)c * ck_stride + (long long)(cb0 + u) * D * B;
-      const bool ok = u == 0 ? valid : ok1;
+      const bool ok = valid && u < nbw;
 #pragma unroll
       for (int i = 0; i < D; ++i) vn[u][i] = ok ? ck[(long long)i * B] : 0.0;
     }
@@ -410,7 +411,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
 #pragma unroll
       for (int u = 0; u < BPW; ++u) {
         const IO* src = dzc + ((long long)(cb0 + u) * TmD + t0) * B + b;
-        const bool ok = u == 0 ? valid : ok1;
+        const bool ok = valid && u < nbw;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           dzn[u][k] = (ok && (!TAIL || t0 + k < TmD)) ? *src : IO(0);
@@ -511,7 +512,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
 #pragma unroll
           for (int i = D - 1; i >= 1; --i) zw[u][i] = zw[u][i - 1];
           zw[u][0] = z;
-          const bool ok = u == 0 ? valid : ok1;
+          const bool ok = valid && u < nbw;
           const bool in_t = !TAIL || t < T;
           const bool in_dz = !TAIL || t < TmD;
           if (!BWD) {
@@ -520,11 +521,11 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
           } else {
             if (sizeof(IO) == 4 && PD && !IRR) {  // (as the single-series kernels of each grid)
               if (ok && in_t) *o0[u] = wio * from_f64<IO>(z);
-              if (u == 0 || two) ls += to_f64<IO>(-(from_f64<IO>(dz) * dzv[u][k]));
+              if (u < nbw) ls += to_f64<IO>(-(from_f64<IO>(dz) * dzv[u][k]));
             } else {
               if (ok && in_t) *o0[u] = from_f64<IO>(to_f64<IO>(wio) * z);
               const double g = -dz * to_f64<IO>(dzv[u][k]);
-              if (u == 0 || two) {
+              if (u < nbw) {
                 if (PD) ls += g;
                 else if (in_dz) lam_acc += g;
               }
