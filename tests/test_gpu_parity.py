@@ -571,6 +571,10 @@ def test_edge_T_all_entry_points(T):
     wsb = P.Workspace(d, T, B, torch.float64, True, C=3)
     zb = torch.empty_like(xb["y"])
     P.whit_forward_bands(xb["y"], xb["w"], xb["lam"], d, T, B, 3, zb, wsb)
+    # bands on uneven dates
+    wtb = P.Workspace(d, T, B, torch.float64, True, C=3, times=True)
+    ztb = torch.empty_like(xb["y"])
+    P.whit_forward_times_bands(xb["y"], xb["w"], xb["lam"], tt, d, T, B, 3, ztb, wtb)
     torch.cuda.synchronize()
     th = tt.cpu().numpy().T
     for b in range(B):
@@ -585,6 +589,9 @@ def test_edge_T_all_entry_points(T):
         ob = O1.forward_backward_bands(Y, xb["w"][:, b].cpu().numpy(), xb["lam"][:, b].cpu().numpy(), d, np.zeros_like(Y))
         for c in range(3):
             assert np.max(np.abs(zb[c, :, b].cpu().numpy() - ob["z"][c].astype(float))) <= 1e-10 * max(1.0, np.abs(Y).max())
+            otb = O1.forward_backward_times(Y[c], xb["w"][:, b].cpu().numpy(), xb["lam"][:, b].cpu().numpy(), th[b], d,
+                                            np.zeros(T))["z"].astype(float)
+            assert np.max(np.abs(ztb[c, :, b].cpu().numpy() - otb)) <= 1e-10 * max(1.0, np.abs(Y).max())
 
 
 def test_lambda_stress_range():
