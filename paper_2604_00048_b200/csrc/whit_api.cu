@@ -42,15 +42,15 @@ using whit_detail::fail;
 namespace {
 
 // chunk length = TMA tile rows (whit::Tile<IO, d>::K)
-int chunk_k(int d) { return d <= 2 ? whit::Tile<float, 2, false>::K : 8; }
+int chunk_k(int d) { return d <= 2 ? whit::Tile<float, 2, false>::K : whit::Tile<float, 3, false>::K; }
 // rows per chunk of the shared-factor multi-band kernel (MB2Layout::K)
 int chunk_k_bands(int d, int nb) {
   if (nb <= 1) return chunk_k(d);
   return d == 1 ? whit::MB2Layout<1, float, true, false>::K
                 : d == 2 ? whit::MB2Layout<2, float, true, false>::K : whit::MB2Layout<3, float, true, false>::K;
 }
-static_assert(whit::Tile<float, 1, false>::K == whit::Tile<double, 2, true>::K && whit::Tile<float, 3, false>::K == 8 &&
-                  whit::Tile<double, 3, true>::K == 8,
+static_assert(whit::Tile<float, 1, false>::K == whit::Tile<double, 2, true>::K &&
+                  whit::Tile<float, 3, false>::K == whit::Tile<double, 3, true>::K,
               "chunk length table out of sync with whit::Tile");
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }

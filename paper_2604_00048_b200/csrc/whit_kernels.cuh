@@ -300,8 +300,11 @@ template <int D> struct Ck {
 #ifndef WHIT_BWD_WARPS
 #define WHIT_BWD_WARPS 2
 #endif
+#ifndef WHIT_TILE_K3
+#define WHIT_TILE_K3 12
+#endif
 template <typename IO, int D, bool BWD> struct Tile {
-  static constexpr int K = D <= 2 ? WHIT_TILE_K2 : 8;
+  static constexpr int K = D <= 2 ? WHIT_TILE_K2 : WHIT_TILE_K3;
   static constexpr int ST = 2;
   static constexpr int WARPS = BWD ? WHIT_BWD_WARPS : 4;
   static constexpr int MAXREG = BWD ? WHIT_BWD_MAXREG : WHIT_FWD_MAXREG;  // SMSP register files (16K): 3 warps/SMSP need <= 168
@@ -580,8 +583,11 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   // WB: the chunk's mask bits, prefetched one chunk ahead (plain coalesced 4-B loads)
   auto wword = [&](int cc) -> uint32_t {
     if (!WB || !valid || cc < 0 || cc >= C) return 0u;
-    const uint32_t word = p.wbits[(long long)((cc * K) >> 5) * B + b];
-    return (word >> ((cc * K) & 31)) & (K >= 32 ? 0xffffffffu : ((1u << K) - 1u));
+    // bits cc*K .. cc*K+K-1 of the series' mask; a chunk may straddle two words when K does not divide 32
+    const int bit0 = cc * K, r = bit0 >> 5, sh = bit0 & 31;
+    uint64_t two = p.wbits[(long long)r * B + b];
+    if (sh + K > 32 && (r + 1) * 32 < T) two |= (uint64_t)p.wbits[(long long)(r + 1) * B + b] << 32;
+    return (uint32_t)(two >> sh) & (K >= 32 ? 0xffffffffu : ((1u << K) - 1u));
   };
   uint32_t wm_next = wword(0);
 
