@@ -321,12 +321,9 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   static constexpr int OFF_LW = OFF_DZ + (BWD ? K * ROW : 0);  // LOSS (forward): loss-weight tile
   static constexpr int STAGE = (OFF_LW + (LOSS ? K * ROW : 0) + 127) / 128 * 128;
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
-  // backward: grad_y staged in the stage's g slot, grad_lambda in its D z slot (both consumed)
-  static constexpr bool INPLACE = false;  // in-place backward staging measured slower (both kernels DRAM-bound)
-  // backward: grad_y and grad_lambda go straight to HBM with coalesced 128-B warp stores (no
-  // staging): 16.9 KB of smem per warp, so 12 warps/SM fit (latency hiding under the power cap)
-  static constexpr bool DIRECT = false;  // measured: no gain over TMA-staged stores at 8 warps (DRAM/power-bound), homo slower
-  static constexpr int WARP_SMEM = ST * STAGE + ((INPLACE || DIRECT) ? 0 : (LOSS ? 3 : 2) * OUT);
+  // outputs are staged per chunk and written by TMA tensor stores (staging in the consumed input slots,
+  // and direct 128-B warp stores, were measured no faster: DESIGN.md §5)
+  static constexpr int WARP_SMEM = ST * STAGE + (LOSS ? 3 : 2) * OUT;
   static constexpr int SMEM = WARPS * WARP_SMEM;
   static constexpr uint32_t BYTES_UP = ((WB ? 1 : 2) * K + (PD ? K : 0)) * ROW;
   static constexpr uint32_t BYTES_DN = ((WB ? 1 : 2) * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
@@ -446,8 +443,7 @@ struct Sweep {
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
-                                                    double two_over_T = 0.0, uint32_t wm = 0, IO* gy0 = nullptr,
-                                                    IO* gl0 = nullptr, long long Bst = 0, bool valid = false) {
+                                                    double two_over_T = 0.0, uint32_t wm = 0) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -514,13 +510,8 @@ struct Sweep {
           if (PD) gl = from_f64<IO>(g);
           else if (!RAGGED || t < TmD) lam_acc += g;
         }
-        if (L::DIRECT) {
-          if (valid && (!RAGGED || t < T)) gy0[(long long)k * Bst] = gy;
-          if (PD && valid && (!RAGGED || t < TmD)) gl0[(long long)k * Bst] = gl;
-        } else {
-          so0[k * 32] = gy;
-          if (PD) so1[k * 32] = gl;
-        }
+        so0[k * 32] = gy;
+        if (PD) so1[k * 32] = gl;
       }
     }
 #pragma unroll
@@ -555,7 +546,7 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   const long long b = bw + lane;
   const bool valid = b < B;
   unsigned char* ring = smem + warp * L::WARP_SMEM;
-  IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);             // forward staging (not INPLACE)
+  IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);             // output staging
   IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
   IO* so2 = reinterpret_cast<IO*>(ring + ST * L::STAGE + 2 * L::OUT);  // LOSS only
   uint64_t* bars = full_bar[warp];
@@ -696,25 +687,18 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
     if (c > 0) WHIT_LOAD_CK(c - 1);
 
     // the staging tiles must have been read by the previous chunk's TMA stores
-    if (!L::INPLACE && !L::DIRECT) {
-      if (lane == 0) bulk_wait_read0();
-      __syncwarp();
-    } else if (L::INPLACE) {
-      so0 = reinterpret_cast<IO*>(const_cast<unsigned char*>(stg) + L::OFF_RHS);
-      so1 = reinterpret_cast<IO*>(const_cast<unsigned char*>(stg) + L::OFF_DZ);
-    }
+    if (lane == 0) bulk_wait_read0();
+    __syncwarp();
     const double two_over_T = 2.0 / (double)T;
-    IO* gy0 = L::DIRECT ? reinterpret_cast<IO*>(p.out0) + (long long)t0 * B + b : nullptr;
-    IO* gl0 = L::DIRECT && PD ? reinterpret_cast<IO*>(p.out1) + (long long)t0 * B + b : nullptr;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    so2 + lane, two_over_T, wm, gy0, gl0, B, valid);
+                                    so2 + lane, two_over_T, wm);
     else
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   so2 + lane, two_over_T, wm, gy0, gl0, B, valid);
+                                   so2 + lane, two_over_T, wm);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
-    if (lane == 0 && !L::DIRECT) {
+    if (lane == 0) {
       tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
       if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
       if (LOSS) tma_store_3d(&p.tm_out2, so2, (int)bw, t0, 0);
@@ -723,7 +707,6 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
     }
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
-      if (L::INPLACE) bulk_wait_read0();  // the stores read this very stage
       fence_proxy_async_smem();
       issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
     }

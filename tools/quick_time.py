@@ -39,4 +39,4 @@ bwd_b = steps * esz * (2 * (3 if pd else 2) + 1 + 1 + (1 if pd else 0)) + C * B 
 tfm, tbm = min(tf), min(tb)
 print(f"{cfg} {dtype} wbits={WB} T={T} B={B}: fwd {tfm:.3f} ms ({fwd_b/tfm/1e6:.0f} GB/s)  bwd {tbm:.3f} ms ({bwd_b/tbm/1e6:.0f} GB/s)  "
       f"fwd+bwd {(tfm+tbm):.3f} ms -> {B/((tfm+tbm)/1e3)/1e6:.2f} M series/s  all: {[round(a,3) for a in tf]} {[round(a,3) for a in tb]}")
-print("nfail", P.whit_failures(ws))
+print("nfail", P.whit_failures(ws), flush=True)
