@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="series in the CPU-oracle sample (0 = auto)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak (default): the config's B series per GPU; strong: B series for the whole job, "
+                         "split over the ranks (fwdbwd op)")
     ap.add_argument("--dist-smoke", action="store_true",
                     help="initialise the NCCL process group even at world size 1 (under torchrun) so the "
                          "barrier / all_reduce / all_gather paths of the multi-GPU run execute on one GPU")
@@ -64,9 +67,15 @@ def dist_env():
     return ws, rank, local
 
 
-def shard(rank: int, world: int, B_per_rank: int):
-    """Weak scaling: rank r owns the global series [r*B, (r+1)*B) (contiguous, disjoint)."""
-    return rank * B_per_rank, B_per_rank
+def shard(rank: int, world: int, B: int, strong: bool = False):
+    """Weak scaling (default): B is per rank and rank r owns the global series [r*B, (r+1)*B).
+    Strong scaling: B is the job total, split into contiguous ranges of a multiple of 4 series
+    (the fp32 row-stride rule), the last rank taking the remainder.  Returns (offset, count)."""
+    if not strong:
+        return rank * B, B
+    per = (B // world) // 4 * 4
+    off = rank * per
+    return off, (B - off if rank == world - 1 else per)
 
 
 def max_over_ranks(value: float, device=None) -> float:
@@ -316,7 +325,9 @@ def run_libwhit(args):
     esz = 4 if io == torch.float32 else 8
     B, T, d = cfg.B, cfg.T, cfg.d
     per_date = cfg.lam_mode == "per_date"
-    off, B = shard(rank, ws_n, B)
+    strong = args.scaling == "strong" and args.op == "fwdbwd"
+    B_job = B if strong else ws_n * B
+    off, B = shard(rank, ws_n, B, strong)
     x = synth.make_inputs(cfg, B=B, series_offset=off, device=dev, dtype=io)
     y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
     stream = torch.cuda.current_stream(dev)
@@ -368,7 +379,7 @@ def run_libwhit(args):
     fwd_ms = [e[0].elapsed_time(e[1]) for e in ev]
     bwd_ms = [e[1].elapsed_time(e[2]) for e in ev]
     ms_step = max_over_ranks(total_ms / K, dev)
-    value = ws_n * B / (ms_step / 1e3)
+    value = B_job / (ms_step / 1e3)
 
     # per-rank checksums of the outputs (exact: int64 sums of the bit patterns, order-independent), gathered
     # over NCCL outside the timed region.  Rank r owns global series [r*B, (r+1)*B) at every N, so rank r's
@@ -417,7 +428,7 @@ def run_libwhit(args):
         ba = statistics.mean(e[1].elapsed_time(e[2]) for e in evb)
         domb, dms, dbytes = ("whit_backward", ba, bbb) if ba >= fa else ("whit_forward_wbits", fa, fbb)
         ach = dbytes / (dms / 1e3) / 1e9
-        wbits_line = {"value": ws_n * B / (msb / 1e3), "unit": UNIT, "ms_per_step": msb,
+        wbits_line = {"value": B_job / (msb / 1e3), "unit": UNIT, "ms_per_step": msb,
                       "w_format": "uint32 bit planes [ceil(T/32)][B] (binary W, P:26), whit_forward_wbits",
                       "gpu_launches": 2 * K,
                       "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
@@ -433,9 +444,9 @@ def run_libwhit(args):
         bits_h = P.whit_pack_mask(w).cpu() if args.config == "hetero" else None
         del wsp, z, gy, gl
         torch.cuda.empty_cache()
-        e2e = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps)
+        e2e = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, B_job=B_job)
         if bits_h is not None:
-            e2e_wbits = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, wbits=bits_h)
+            e2e_wbits = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, wbits=bits_h, B_job=B_job)
 
     # CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
@@ -453,10 +464,11 @@ def run_libwhit(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws_n, "steps": K, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "B_per_gpu": B, "T": T, "d": d, "lambda": cfg.lam_mode,
-                       "io": args.io, "global_batch": ws_n * B, "parallelism": f"dp{ws_n}",
+                       "io": args.io, "global_batch": B_job, "parallelism": f"dp{ws_n}",
                        "l2": "inputs larger than L2 (each [T][B] plane %.2f GB vs 126 MB L2)" % (T * B * esz / 1e9),
                        "mask": "Sentinel-2 revisit + seasonal clouds, 90-day trailing gap",
                        "failed_series": nfail},
@@ -647,7 +659,7 @@ def run_s2tile(args, P, synth, dev, ws_n, rank):
     return 0
 
 
-def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6, wbits=None):
+def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6, wbits=None, B_job=None):
     """Same metric through the public C-ABI with pinned HOST buffers: whit_run_host streams the
     batch in series chunks (pitched 2-D H2D copies of y, w, lambda, g; whit_forward +
     whit_backward; D2H of z, grad_y, grad_lambda), copies overlapping kernels on nbuf streams.
@@ -681,7 +693,8 @@ def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6, wbits=Non
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(e0.elapsed_time(e1) / steps, dev)
-    return {"value": ws_n * B / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+    return {"value": (B_job or ws_n * B) / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h,
             "ms_per_step": ms, "steps": steps,
             "api": f"{'whit_run_host_wbits' if bits is not None else 'whit_run_host'} (C-ABI, pinned host buffers, "
                    f"chunk {chunk}, {nbuf} streams)"}

@@ -65,6 +65,16 @@ def test_world2_shards_timing_and_rank_independent_inputs():
     assert [a + b for a, b in zip(*cks["per_rank"])] == tot
 
 
+def test_strong_scaling_shards_cover_the_job():
+    """--scaling strong: contiguous ranges of multiples of 4 series covering [0, B) exactly once."""
+    import bench
+    for B, world in ((262144, 8), (65536, 3), (1000, 4), (4100, 2)):
+        parts = [bench.shard(r, world, B, strong=True) for r in range(world)]
+        assert parts[0][0] == 0 and sum(n for _, n in parts) == B
+        for (o0, n0), (o1, _) in zip(parts, parts[1:]):
+            assert o0 + n0 == o1 and n0 % 4 == 0
+
+
 def test_max_over_ranks_without_group_is_identity():
     import bench
     assert bench.max_over_ranks(3.25) == 3.25
