@@ -236,6 +236,39 @@ def oracle_rate(hin: dict, n: int, d: int, pool):
     return n / wall, wall, sum(per)
 
 
+def _banded_one(args):
+    """One series, fwd+bwd, with a conventional CPU banded solver (LAPACK pbsv via scipy's
+    solveh_banded, fp64): the context baseline beside the oracle; not the oracle, not the product."""
+    import numpy as np
+    from scipy.linalg import solveh_banded
+    y, w, lam, g, d = args
+    t = time.perf_counter()
+    T = y.shape[0]
+    c = np.array([(-1) ** (d - j) * __import__("math").comb(d, j) for j in range(d + 1)], dtype=np.float64)
+    lt = np.zeros(T)
+    lt[:T - d] = lam if np.ndim(lam) else lam
+    ab = np.zeros((d + 1, T))  # upper band storage: ab[d + i - j, col j] = Omega[row i, col j]
+    ab[d] = w.copy()
+    for i in range(d + 1):  # Omega[r+i, r+j] += lambda_r c_i c_j over the difference rows r
+        for j in range(i, d + 1):
+            ab[d + i - j, j:j + T - d] += lt[:T - d] * (c[i] * c[j])
+    b = np.where(w != 0, w * np.nan_to_num(y), 0.0)
+    z = solveh_banded(ab, b)
+    u = solveh_banded(ab, g)
+    dz = np.convolve(z, c[::-1], "valid")
+    du = np.convolve(u, c[::-1], "valid")
+    _ybar, _lbar = w * u, -du * dz
+    return time.perf_counter() - t
+
+
+def banded_rate(hin: dict, n: int, d: int, pool):
+    items = [(hin["y"][i], hin["w"][i], hin["lam"][i], hin["g"][i], d) for i in range(n)]
+    t0 = time.perf_counter()
+    pool.map(_banded_one, items, chunksize=max(1, n // (4 * (pool._processes or 1))))
+    wall = time.perf_counter() - t0
+    return n / wall, wall
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -448,18 +481,27 @@ def run_libwhit(args):
         if bits_h is not None:
             e2e_wbits = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, wbits=bits_h, B_job=B_job)
 
-    # CPU oracle baseline (rank 0, N = 1 only)
+    # CPU oracle baseline (rank 0, N = 1 only), and a conventional CPU banded solver for context
     cpu = None
+    cpu_banded = None
     if rank == 0 and ws_n == 1 and not args.no_cpu_baseline:
         cores = min(host_cores(), 32)
         n = args.cpu_sample or 2 * cores
         hin = sample_host_inputs(x, n)
         pool = oracle_pool(cores)
         rate, wall, cpu_s = oracle_rate(hin, n, d, pool)
+        nb = 256 * cores
+        hb = sample_host_inputs(x, nb)
+        banded_rate(hb, cores, d, pool)  # warm the workers' scipy import
+        brate, bwall = banded_rate(hb, nb, d, pool)
         pool.close()
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{n} series of this workload (spread over the batch), O1 dense fp64 + long-double "
                          f"refinement, fwd+bwd, {cores} processes, {wall:.1f} s wall / {cpu_s:.1f} s CPU"}
+        cpu_banded = {"value": brate, "unit": UNIT, "cores": cores,
+                      "kind": "context: scipy.linalg.solveh_banded (LAPACK pbsv) fp64, band assembled in numpy, "
+                              "forward + adjoint solve + gradients",
+                      "sample": f"{nb} series of this workload, {cores} processes, {bwall:.2f} s wall"}
 
     if rank == 0:
         line = {
@@ -473,6 +515,7 @@ def run_libwhit(args):
                        "mask": "Sentinel-2 revisit + seasonal clouds, 90-day trailing gap",
                        "failed_series": nfail},
             "roofline": roof, "gpu_launches": 2 * K, "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+            "cpu_banded": cpu_banded,
             "w_bits": wbits_line, "e2e_wbits": e2e_wbits, "checksums": checksums,
         }
         print(json.dumps(line), flush=True)
