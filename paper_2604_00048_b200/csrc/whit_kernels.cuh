@@ -973,8 +973,32 @@ __global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params 
     for (int j = 0; j < D; ++j) { cA[i][j] = 0.0; cM[i][j] = Mj(D, j + 1); }
   }
   double lam_acc = 0.0;
+  // checkpoints of the next chunk, loaded one chunk ahead (their latency leaves the chunk's start)
+  double pck[NFAC], pv[D];
+  auto load_ck = [&](int cc) {
+    const double* ckf = p.ck_fac + (long long)cc * NFAC * B + b;
+    const double* ckr = ck_rhs + (long long)cc * D * B;
+#pragma unroll
+    for (int f = 0; f < NFAC; ++f) pck[f] = valid ? ckf[(long long)f * B] : 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) pv[i] = valid ? ckr[(long long)i * B] : 0.0;
+  };
+  load_ck(C - 1);
   for (int c = C - 1; c >= 0; --c, ++it) {
     const int s = it % ST;
+    // restore the state entering row t0
+    {
+      int f = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) S.f.dl[i] = pck[f++];
+#pragma unroll
+      for (int m = 0; m < D - 1; ++m)
+#pragma unroll
+        for (int k = 0; k < D - 1 - m; ++k) S.f.ap[m][k] = pck[f++];
+#pragma unroll
+      for (int i = 0; i < D; ++i) S.f.v[i] = pv[i] + poison;
+    }
+    if (c > 0) load_ck(c - 1);
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const unsigned char* stg = ring + s * L::STAGE;
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
@@ -983,20 +1007,6 @@ __global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params 
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
     const IO* t_dz = reinterpret_cast<const IO*>(stg + L::OFF_DZ) + lane;
     const int t0 = c * K;
-    // restore the state entering row t0
-    if (valid) {
-      const double* ckf = p.ck_fac + (long long)c * NFAC * B + b;
-      int f = 0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) S.f.dl[i] = ckf[(long long)(f++) * B];
-#pragma unroll
-      for (int m = 0; m < D - 1; ++m)
-#pragma unroll
-        for (int k = 0; k < D - 1 - m; ++k) S.f.ap[m][k] = ckf[(long long)(f++) * B];
-      const double* ckr = ck_rhs + (long long)c * D * B;
-#pragma unroll
-      for (int i = 0; i < D; ++i) S.f.v[i] = ckr[(long long)i * B] + poison;
-    }
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       const int tj = t0 - 1 - i;
