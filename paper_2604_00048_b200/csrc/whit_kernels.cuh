@@ -1209,24 +1209,31 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
   for (int i = 0; i < D; ++i)
 #pragma unroll
     for (int j = 0; j < D; ++j) { cA[i][j] = 0.0; S[i][j] = poison; }
+  double pck[NFAC];  // the next chunk's factor checkpoint, loaded one chunk ahead
+  auto load_ck = [&](int cc) {
+    const double* ckf = p.ck_fac + (long long)cc * NFAC * B + b;
+#pragma unroll
+    for (int f = 0; f < NFAC; ++f) pck[f] = valid ? ckf[(long long)f * B] : 0.0;
+  };
+  load_ck(C - 1);
   for (int c = C - 1; c >= 0; --c, ++it) {
     const int s = it % ST;
+    {
+      int f = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) st.dl[i] = pck[f++];
+#pragma unroll
+      for (int m = 0; m < D - 1; ++m)
+#pragma unroll
+        for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = pck[f++];
+    }
+    if (c > 0) load_ck(c - 1);
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const unsigned char* stg = ring + s * V::STAGE;
     const IO* t_w = reinterpret_cast<const IO*>(stg + V::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + V::OFF_LAM) + lane;  // row k <-> t0 - D + k
     const int t0 = c * K;
     const bool ragged = (t0 + K > T);
-    if (valid) {
-      const double* ckf = p.ck_fac + (long long)c * NFAC * B + b;
-      int f = 0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) st.dl[i] = ckf[(long long)(f++) * B];
-#pragma unroll
-      for (int m = 0; m < D - 1; ++m)
-#pragma unroll
-        for (int k = 0; k < D - 1 - m; ++k) st.ap[m][k] = ckf[(long long)(f++) * B];
-    }
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       const int tj = t0 - 1 - i;
