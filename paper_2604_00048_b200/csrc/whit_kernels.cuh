@@ -1155,7 +1155,6 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
   }
   __syncwarp();
   const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
-  const int cr = (T - D) / K;
 
   FState<D> st;
   state_init<D>(st);
