@@ -856,3 +856,36 @@ def test_bands_degenerate_pixels(times):
     z2, gy2, gl2, _, _ = run(w2)
     assert torch.equal(z[:, :, ok], z2[:, :, ok]) and torch.equal(gy[:, :, ok], gy2[:, :, ok])
     assert torch.equal(gl[:, ok], gl2[:, ok])
+
+
+@pytest.mark.parametrize("times", [False, True])
+def test_bands_lambda_stress_finite_and_consistent(times):
+    """Multi-band paths at the lambda extremes the network can emit (1e-6 .. 1e10): finite results,
+    and z / grad_y bitwise equal to the matching single-band path."""
+    import paper_2604_00048_b200 as P
+
+    d, C, T, B = 2, 3, 260, 64
+    x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, device="cuda", seed=91)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    loglam = torch.empty(T - d, B).uniform_(-6, 10, generator=g)
+    lam = (10.0 ** loglam).float().cuda()
+    tt = synth.make_times(B, T, device="cuda") if times else None
+    ws = P.Workspace(d, T, B, torch.float32, True, C=C, times=times)
+    z, gy, gl = torch.empty_like(x["y"]), torch.empty_like(x["y"]), torch.empty_like(lam)
+    if times:
+        P.whit_forward_times_bands(x["y"], x["w"], lam, tt, d, T, B, C, z, ws)
+    else:
+        P.whit_forward_bands(x["y"], x["w"], lam, d, T, B, C, z, ws)
+    P.whit_backward_bands(x["g"], ws, z, gy, gl)
+    assert P.whit_failures(ws) == 0
+    for t in (z, gy, gl):
+        assert bool(torch.isfinite(t).all())
+    ws1 = P.Workspace(d, T, B, torch.float32, True, times=times)
+    for c in range(C):
+        z1, gy1, gl1 = torch.empty_like(x["y"][c]), torch.empty_like(x["y"][c]), torch.empty_like(lam)
+        if times:
+            P.whit_forward_times(x["y"][c].contiguous(), x["w"], lam, tt, d, T, B, z1, ws1)
+        else:
+            P.whit_forward(x["y"][c].contiguous(), x["w"], lam, d, T, B, z1, ws1)
+        P.whit_backward(x["g"][c].contiguous(), ws1, z1, gy1, gl1)
+        assert torch.equal(z[c], z1) and torch.equal(gy[c], gy1), c
