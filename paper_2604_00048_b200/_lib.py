@@ -162,6 +162,13 @@ def _shapes(ws: "Workspace", where: str, lam, *planes, C: int = 1):
     """Tensor-shape checks the pointer ABI cannot make: lambda's mode must match the workspace
     ((T-d, B) per date, (B,) scalar) and the [T][B] / [C][T][B] planes must have the workspace's shape."""
     T, B, d = ws.T, ws.B, ws.d
+    for name, t in [("lambda", lam)] + [(n, t) for n, t, _ in planes]:
+        if not t.is_contiguous():
+            raise ValueError(f"{where}: {name} must be contiguous (the ABI reads a dense [T][B] plane)")
+        if t.dtype != ws.dtype:
+            raise TypeError(f"{where}: {name} dtype {t.dtype} != workspace dtype {ws.dtype}")
+        if getattr(ws, "device_check", True) and not t.is_cuda:
+            raise ValueError(f"{where}: {name} must be a CUDA tensor (no CPU fallback)")
     want = (T - d, B) if ws.per_date else (B,)
     if tuple(lam.shape) != want:
         raise ValueError(f"{where}: lambda shape {tuple(lam.shape)} != {want} "

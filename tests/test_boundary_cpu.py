@@ -119,14 +119,18 @@ def test_python_binding_rejects_mismatched_lambda_mode_and_shapes():
     import torch
     from paper_2604_00048_b200 import _lib as L
 
-    ws = types.SimpleNamespace(T=50, B=8, d=2, C=1, per_date=True)
+    ws = types.SimpleNamespace(T=50, B=8, d=2, C=1, per_date=True, dtype=torch.float32, device_check=False)
     y = torch.zeros(50, 8)
     with pytest.raises(ValueError, match="lambda shape"):
         L._shapes(ws, "whit_forward", torch.zeros(8), ("y", y, "TB"))
     with pytest.raises(ValueError, match="y shape"):
         L._shapes(ws, "whit_forward", torch.zeros(48, 8), ("y", torch.zeros(49, 8), "TB"))
     L._shapes(ws, "whit_forward", torch.zeros(48, 8), ("y", y, "TB"))
-    ws3 = types.SimpleNamespace(T=50, B=8, d=2, C=3, per_date=False)
+    with pytest.raises(ValueError, match="contiguous"):
+        L._shapes(ws, "whit_forward", torch.zeros(48, 8), ("y", torch.zeros(8, 50).t(), "TB"))
+    with pytest.raises(TypeError, match="dtype"):
+        L._shapes(ws, "whit_forward", torch.zeros(48, 8), ("y", torch.zeros(50, 8, dtype=torch.float64), "TB"))
+    ws3 = types.SimpleNamespace(T=50, B=8, d=2, C=3, per_date=False, dtype=torch.float32, device_check=False)
     L._shapes(ws3, "whit_forward_bands", torch.zeros(8), ("y", torch.zeros(3, 50, 8), "CTB"), C=3)
     with pytest.raises(ValueError):
         L._shapes(ws3, "whit_forward_bands", torch.zeros(8), ("y", torch.zeros(2, 50, 8), "CTB"), C=3)
