@@ -78,6 +78,11 @@ def shard(rank: int, world: int, B: int, strong: bool = False):
     return off, (B - off if rank == world - 1 else per)
 
 
+def dist_is_init() -> bool:
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized()
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar over the default process group (identity without one)."""
     import torch
@@ -689,6 +694,36 @@ def run_s2tile(args, P, synth, dev, ws_n, rank):
     clocks = clk.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dev)
     nfail = P.whit_failures(wsp)
+    # end to end from pinned HOST memory through whit_run_host_bands (pixel chunks streamed through the
+    # shared-factor kernels, copies overlapped with compute)
+    e2e = None
+    if not args.no_e2e:
+        del wsp, z, gy, gl
+        torch.cuda.empty_cache()
+        h = {k: torch.empty(x[k].shape, dtype=torch.float32, pin_memory=True) for k in ("y", "w", "lam", "g")}
+        for k in h:
+            h[k].copy_(x[k])
+        oz = torch.empty(h["y"].shape, dtype=torch.float32, pin_memory=True)
+        oy = torch.empty(h["y"].shape, dtype=torch.float32, pin_memory=True)
+        ol = torch.empty(h["lam"].shape, dtype=torch.float32, pin_memory=True)
+        buf = P.whit_run_host_bands(h["y"], h["w"], h["lam"], h["g"], d, oz, oy, ol, chunk=4096, nbuf=4,
+                                    stream=stream)
+        torch.cuda.synchronize(dev)
+        if dist_is_init():
+            import torch.distributed as dist
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            P.whit_run_host_bands(h["y"], h["w"], h["lam"], h["g"], d, oz, oy, ol, chunk=4096, nbuf=4, dev_buf=buf,
+                                  stream=stream)
+        f1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, dev)
+        e2e = {"value": ws_n * Bp * C / (ems / 1e3), "unit": "band-series/s",
+               "h2d_bytes_per_step": sum(t.numel() * 4 for t in h.values()),
+               "d2h_bytes_per_step": sum(t.numel() * 4 for t in (oz, oy, ol)), "ms_per_step": ems,
+               "steps": args.e2e_steps, "api": "whit_run_host_bands (C-ABI, pinned host buffers, chunk 4096, 4 streams)"}
     if rank == 0:
         print(json.dumps({
             "metric": "band-series fwd+bwd solves/s (Sentinel-2 tile chunk, shared factor per pixel)",
@@ -698,7 +733,8 @@ def run_s2tile(args, P, synth, dev, ws_n, rank):
             "config": {"workload": "s2tile", "bands": C, "pixels_per_gpu": Bp, "tile_pixels": 1048576, "T": T,
                        "d": d, "lambda": "per_date", "io": "f32", "parallelism": f"dp{ws_n}",
                        "l2": "inputs larger than L2", "failed_series": nfail},
-            "pixels_per_s": ws_n * Bp / (ms / 1e3), "gpu_launches": 2 * args.steps, "clocks": clocks}), flush=True)
+            "pixels_per_s": ws_n * Bp / (ms / 1e3), "gpu_launches": 2 * args.steps, "clocks": clocks,
+            "e2e": e2e}), flush=True)
     return 0
 
 

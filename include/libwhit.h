@@ -327,6 +327,19 @@ whit_status whit_run_host_wbits(const void* y, const uint32_t* wbits, const void
                                 void* grad_y, void* grad_lambda, int32_t* info, int64_t chunk, int nbuf,
                                 void* dev_buf, size_t dev_bytes, void* cuda_stream);
 
+/* Multi-band pixels from HOST memory (a Sentinel-2 tile streamed through the
+ * shared-factor kernels): y, grad_z, z, grad_y are HOST [C][T][B] (band planes
+ * stacked), w [T][B] and lambda shared, info per pixel; each chunk of `chunk`
+ * pixels runs whit_forward_bands (+ whit_backward_bands).  Device scratch:
+ * whit_host_ws_bytes_bands (C = 1 gives whit_host_ws_bytes). */
+size_t whit_host_ws_bytes_bands(int d, int64_t T, int64_t chunk, int C, whit_dtype dtype,
+                                whit_lambda_mode lambda_mode, int nbuf);
+
+whit_status whit_run_host_bands(const void* y, const void* w, const void* lambda, const void* grad_z, int d,
+                                int64_t T, int64_t B, int C, whit_dtype dtype, whit_lambda_mode lambda_mode,
+                                void* z, void* grad_y, void* grad_lambda, int32_t* info, int64_t chunk, int nbuf,
+                                void* dev_buf, size_t dev_bytes, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,10 @@ SIGNATURES = [
                                      _VP, _VP, _VP, _VP, _I64, ctypes.c_int, _VP, _SZ, _VP]),
     ("whit_run_host_wbits", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                            _VP, _VP, _VP, _VP, _I64, ctypes.c_int, _VP, _SZ, _VP]),
+    ("whit_host_ws_bytes_bands", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int]),
+    ("whit_run_host_bands", ctypes.c_int, [_VP, _VP, _VP, _VP, ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, _VP, _VP, _VP, _VP, _I64, ctypes.c_int, _VP, _SZ, _VP]),
 ]
 
 
@@ -262,6 +266,27 @@ def whit_failures(ws: Workspace, with_info: bool = False):
 
 def whit_host_ws_bytes(d: int, T: int, chunk: int, dtype, per_date: bool, nbuf: int) -> int:
     return int(_lib.whit_host_ws_bytes(d, T, chunk, _dtype_code(dtype), int(per_date), nbuf))
+
+
+def whit_run_host_bands(y, w, lam, grad_z, d: int, z, grad_y=None, grad_lambda=None, info=None, *,
+                        chunk: int = 8192, nbuf: int = 3, dev_buf=None, stream=None):
+    """Streaming executor for C bands per pixel in HOST memory: y, grad_z, z, grad_y (C, T, B); w (T, B);
+    lam (T-d, B) or (B,).  Returns the device buffer (reuse it across calls)."""
+    C, T, B = y.shape
+    per_date = lam.dim() == 2
+    need = int(_lib.whit_host_ws_bytes_bands(d, T, min(chunk, B), C, _dtype_code(y.dtype), int(per_date), nbuf))
+    if need == 0:
+        raise WhitError(1, "whit_host_ws_bytes_bands")
+    if dev_buf is None or dev_buf.numel() < need:
+        dev_buf = torch.empty(need, dtype=torch.uint8, device="cuda")
+    for t in (y, w, lam, z) + ((grad_z, grad_y, grad_lambda) if grad_z is not None else ()):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("whit_run_host_bands takes contiguous HOST tensors")
+    _check(_lib.whit_run_host_bands(_ptr(y), _ptr(w), _ptr(lam), _ptr(grad_z), d, T, B, C, _dtype_code(y.dtype),
+                                    int(per_date), _ptr(z), _ptr(grad_y), _ptr(grad_lambda), _ptr(info),
+                                    min(chunk, B), nbuf, ctypes.c_void_p(dev_buf.data_ptr()), dev_buf.numel(),
+                                    _stream_handle(stream)), "whit_run_host_bands")
+    return dev_buf
 
 
 def whit_run_host(y, w, lam, grad_z, d: int, z, grad_y=None, grad_lambda=None, info=None, *, chunk: int = 16384,

@@ -889,3 +889,25 @@ def test_bands_lambda_stress_finite_and_consistent(times):
             P.whit_forward(x["y"][c].contiguous(), x["w"], lam, d, T, B, z1, ws1)
         P.whit_backward(x["g"][c].contiguous(), ws1, z1, gy1, gl1)
         assert torch.equal(z[c], z1) and torch.equal(gy[c], gy1), c
+
+
+def test_host_executor_bands_matches_device_path_bitwise():
+    """whit_run_host_bands (C bands per pixel streamed from HOST memory in pixel chunks through the
+    shared-factor kernels) returns exactly the device multi-band entry points' results."""
+    import paper_2604_00048_b200 as P
+
+    d, C, T, B = 2, 4, 200, 1000
+    x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, device="cuda", seed=81)
+    ws = P.Workspace(d, T, B, torch.float32, True, C=C)
+    z, gy, gl = torch.empty_like(x["y"]), torch.empty_like(x["y"]), torch.empty_like(x["lam"])
+    P.whit_forward_bands(x["y"], x["w"], x["lam"], d, T, B, C, z, ws)
+    P.whit_backward_bands(x["g"], ws, z, gy, gl)
+    _, info_dev = P.whit_failures(ws, with_info=True)
+    h = {k: x[k].cpu().pin_memory() for k in ("y", "w", "lam", "g")}
+    hz, hgy = torch.empty_like(h["y"]).pin_memory(), torch.empty_like(h["y"]).pin_memory()
+    hgl = torch.empty_like(h["lam"]).pin_memory()
+    info = torch.empty(B, dtype=torch.int32).pin_memory()
+    P.whit_run_host_bands(h["y"], h["w"], h["lam"], h["g"], d, hz, hgy, hgl, info, chunk=256, nbuf=3)
+    torch.cuda.synchronize()
+    assert torch.equal(hz, z.cpu()) and torch.equal(hgy, gy.cpu()) and torch.equal(hgl, gl.cpu())
+    assert np.array_equal(info.numpy(), info_dev)
