@@ -911,3 +911,43 @@ def test_host_executor_bands_matches_device_path_bitwise():
     torch.cuda.synchronize()
     assert torch.equal(hz, z.cpu()) and torch.equal(hgy, gy.cpu()) and torch.equal(hgl, gl.cpu())
     assert np.array_equal(info.numpy(), info_dev)
+
+
+@pytest.mark.parametrize("C", [1, 10])
+def test_irregular_full_shape_sampled(C):
+    """`bench.py --op irregular` (C = 1: 262,144 series) and `--op table1` (C = 10 bands per pixel) at their
+    benched shapes (T = 350 uneven dates, d = 2, per-date lambda, fp32): sampled series vs O1 on the same dates."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 350, 262144
+    if C == 1:
+        x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", mask="bernoulli")
+        y, g = x["y"][None], x["g"][None]
+    else:
+        x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, device="cuda", mask="bernoulli")
+        y, g = x["y"], x["g"]
+    w, lam = x["w"], x["lam"]
+    tt = synth.make_times(B, T, device="cuda")
+    ws = P.Workspace(d, T, B, torch.float32, True, C=C, times=True)
+    z, gy, gl = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam)
+    if C == 1:
+        P.whit_forward_times(y[0], w, lam, tt, d, T, B, z[0], ws)
+        P.whit_backward(g[0], ws, z[0], gy[0], gl)
+    else:
+        P.whit_forward_times_bands(y, w, lam, tt, d, T, B, C, z, ws)
+        P.whit_backward_bands(g, ws, z, gy, gl)
+    assert P.whit_failures(ws) == 0
+    for t in (z, gy, gl):
+        assert bool(torch.isfinite(t).all())
+    tz, tg = TOL[(torch.float32, d)]
+    for b in _sample(B, 3):
+        wb, lb, tb = (v[:, b].double().cpu().numpy() for v in (w, lam, tt))
+        ref_l = 0.0
+        for c in range(C):
+            yc, gc = y[c, :, b].double().cpu().numpy(), g[c, :, b].double().cpu().numpy()
+            o = O1.forward_backward_times(yc, wb, lb, tb, d, gc)
+            ez = np.max(np.abs(z[c, :, b].double().cpu().numpy() - o["z"].astype(float))) / ymax_observed(yc, wb)
+            assert ez <= tz, (b, c, ez)
+            assert rel_series(gy[c, :, b].double().cpu().numpy(), o["ybar"]).max() <= tg, (b, c)
+            ref_l = ref_l + o["lambar"]
+        assert rel_series(gl[:, b].double().cpu().numpy(), ref_l).max() <= tg, b
