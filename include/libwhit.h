@@ -277,7 +277,7 @@ whit_status whit_posterior_variance(const void* w, const void* lambda, int d, in
                                     whit_ws* factor_ws);
 
 /* SYNCHRONISES the workspace stream, then reports how many series of the
- * last forward failed (non-SPD, see "Numerical failure") in *n_failed and,
+ * last forward (or posterior variance) failed (non-SPD, see "Numerical failure") in *n_failed and,
  * if host_info is non-NULL, copies info[0..B) (int32) to host_info. */
 whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info);
 

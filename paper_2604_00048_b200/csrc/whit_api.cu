@@ -134,7 +134,8 @@ struct whit_ws {
   size_t bytes;
   cudaStream_t stream;
   WsLayout L;
-  bool have_fwd;
+  bool have_fwd;   // a forward ran and its checkpoints are intact (whit_backward may follow)
+  bool have_info;  // info[] holds the status of the last forward or posterior variance
   const void* w;
   const void* lam;
   const void* z;
@@ -499,7 +500,7 @@ static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, 
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
-  ws->have_fwd = false; ws->w = ws->lam = ws->z = nullptr;
+  ws->have_fwd = false; ws->have_info = false; ws->w = ws->lam = ws->z = nullptr;
   ws->device = -1;
   int dev = -1;
   if (cudaGetDevice(&dev) == cudaSuccess) ws->device = dev;
@@ -546,6 +547,7 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   st = dispatch<false>(ws, p);
   if (st != WHIT_OK) return st;
   ws->have_fwd = true;
+  ws->have_info = true;
   ws->w = w; ws->lam = lambda; ws->z = z; ws->wbits = nullptr;
   return WHIT_OK;
 }
@@ -574,6 +576,7 @@ whit_status whit_forward_wbits(const void* y, const uint32_t* wbits, const void*
   st = dispatch_wb<false>(ws, p);
   if (st != WHIT_OK) return st;
   ws->have_fwd = true;
+  ws->have_info = true;
   ws->w = wbits; ws->lam = lambda; ws->z = z; ws->wbits = wbits;
   return WHIT_OK;
 }
@@ -621,6 +624,7 @@ whit_status whit_forward_times_bands(const void* y, const void* w, const void* l
   st = dispatch_irr<false>(ws, p);
   if (st != WHIT_OK) return st;
   ws->have_fwd = true;
+  ws->have_info = true;
   ws->w = w; ws->lam = lambda; ws->z = z; ws->times = times;
   return WHIT_OK;
 }
@@ -663,6 +667,7 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
     st = pd ? dispatch_loss_d<double, true>(d, p, ws->stream) : dispatch_loss_d<double, false>(d, p, ws->stream);
   if (st != WHIT_OK) return st;
   ws->have_fwd = true;
+  ws->have_info = true;
   ws->w = w; ws->lam = lambda; ws->z = z;
   return WHIT_OK;
 }
@@ -756,6 +761,7 @@ whit_status whit_posterior_variance(const void* w, const void* lambda, int d, in
   if ((st = encode_map(&p.tm_out0, var, ws->dt, B, T, ws->kk, 1)) != WHIT_OK) return st;
   // the factor checkpoints are shared with the forward: a different (w, lambda) invalidates its backward
   if (w != ws->w || lambda != ws->lam) ws->have_fwd = false;
+  ws->have_info = true;  // (set at enqueue: info is written by this launch)
   const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
   if (ws->dt == WHIT_F32)
     return pd ? dispatch_var_d<float, true>(d, p, ws->stream) : dispatch_var_d<float, false>(d, p, ws->stream);
@@ -764,7 +770,7 @@ whit_status whit_posterior_variance(const void* w, const void* lambda, int d, in
 
 whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {
   if (!ws || !n_failed) return fail(WHIT_ERR_ARG, "NULL argument");
-  if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "no forward has run on this workspace");
+  if (!ws->have_info) return fail(WHIT_ERR_STATE, "no forward or posterior variance has run on this workspace");
   DeviceGuard guard(ws->device);
   auto* cnt = reinterpret_cast<unsigned long long*>(ws->buf + ws->L.off_cnt);
   const int32_t* info = reinterpret_cast<const int32_t*>(ws->buf + ws->L.off_info);

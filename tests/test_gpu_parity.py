@@ -951,3 +951,25 @@ def test_irregular_full_shape_sampled(C):
             assert rel_series(gy[c, :, b].double().cpu().numpy(), o["ybar"]).max() <= tg, (b, c)
             ref_l = ref_l + o["lambar"]
         assert rel_series(gl[:, b].double().cpu().numpy(), ref_l).max() <= tg, b
+
+
+def test_failures_after_posterior_variance_only():
+    """whit_failures reports the status of a posterior variance run on a fresh workspace (no forward),
+    and a backward after a variance with different (w, lambda) is refused (its checkpoints were overwritten)."""
+    import paper_2604_00048_b200 as P
+
+    d, T, B = 2, 100, 64
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", seed=95)
+    w = x["w"].clone()
+    w[:, 3] = 0.0
+    ws = P.Workspace(d, T, B, torch.float32, True)
+    var = torch.empty_like(w)
+    P.whit_posterior_variance(w, x["lam"], d, T, B, var, ws)
+    n, info = P.whit_failures(ws, with_info=True)
+    assert n == 1 and info[3] == T - d + 1 and bool(torch.isnan(var[:, 3]).all())
+    z = torch.empty_like(x["y"])
+    P.whit_forward(x["y"], x["w"], x["lam"], d, T, B, z, ws)
+    P.whit_posterior_variance(w, x["lam"], d, T, B, var, ws)  # different w: the forward's backward is invalid
+    gy, gl = torch.empty_like(x["y"]), torch.empty_like(x["lam"])
+    with pytest.raises(P.WhitError):
+        P.whit_backward(x["g"], ws, z, gy, gl)
