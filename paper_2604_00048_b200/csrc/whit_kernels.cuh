@@ -300,6 +300,9 @@ template <int D> struct Ck {
 #ifndef WHIT_BWD_WARPS
 #define WHIT_BWD_WARPS 2
 #endif
+#ifndef WHIT_TILE_ST
+#define WHIT_TILE_ST 2
+#endif
 #ifndef WHIT_FWD_WARPS
 #define WHIT_FWD_WARPS 4
 #endif
@@ -308,7 +311,7 @@ template <int D> struct Ck {
 #endif
 template <typename IO, int D, bool BWD> struct Tile {
   static constexpr int K = D <= 2 ? WHIT_TILE_K2 : WHIT_TILE_K3;
-  static constexpr int ST = 2;
+  static constexpr int ST = WHIT_TILE_ST;
   static constexpr int WARPS = BWD ? WHIT_BWD_WARPS : WHIT_FWD_WARPS;
   static constexpr int MAXREG = BWD ? WHIT_BWD_MAXREG : WHIT_FWD_MAXREG;  // SMSP register files (16K): 3 warps/SMSP need <= 168
 };
