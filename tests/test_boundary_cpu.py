@@ -134,3 +134,16 @@ def test_python_binding_rejects_mismatched_lambda_mode_and_shapes():
     L._shapes(ws3, "whit_forward_bands", torch.zeros(8), ("y", torch.zeros(3, 50, 8), "CTB"), C=3)
     with pytest.raises(ValueError):
         L._shapes(ws3, "whit_forward_bands", torch.zeros(8), ("y", torch.zeros(2, 50, 8), "CTB"), C=3)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """Without libwhit.so the package refuses to import (no CPU fallback)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WHIT_LIB_PATH=str(tmp_path / "missing" / "libwhit.so"))
+    out = subprocess.run([sys.executable, "-c", "import paper_2604_00048_b200"], cwd=root, env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode != 0 and "ImportError" in out.stderr and "no CPU fallback" in out.stderr
