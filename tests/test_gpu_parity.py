@@ -973,3 +973,40 @@ def test_failures_after_posterior_variance_only():
     gy, gl = torch.empty_like(x["y"]), torch.empty_like(x["lam"])
     with pytest.raises(P.WhitError):
         P.whit_backward(x["g"], ws, z, gy, gl)
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_randomised_shapes_through_autograd(case):
+    """Seeded random shapes through the autograd shim (arbitrary B: the shim pads to the 16-B row stride):
+    d, T (down to d + 1), B, dtype, lambda mode and mask density drawn per case; z and the gradients vs O1."""
+    import paper_2604_00048_b200 as P
+
+    rng = np.random.default_rng(1000 + case)
+    d = int(rng.integers(1, 4))
+    T = int(rng.integers(d + 1, 260))
+    B = int(rng.integers(1, 70))
+    dtype = torch.float64 if rng.random() < 0.4 else torch.float32
+    per_date = bool(rng.random() < 0.6)
+    dens = float(rng.uniform(0.15, 1.0))
+    y = torch.tensor(rng.normal(size=(T, B)), dtype=dtype, device="cuda", requires_grad=True)
+    w = (rng.random((T, B)) < dens).astype(float)
+    w[rng.integers(0, T, size=(d + 1,)), :] = 1.0  # at least d observed days somewhere...
+    w[:d + 1, :] = 1.0                              # ... and surely
+    w = torch.tensor(w, dtype=dtype, device="cuda")
+    lam_np = 10 ** rng.uniform(0, 4, size=(T - d, B) if per_date else (B,))
+    lam = torch.tensor(lam_np, dtype=dtype, device="cuda", requires_grad=True)
+    g = torch.tensor(rng.normal(size=(T, B)), dtype=dtype, device="cuda")
+    z = P.smooth(y, w, lam, d)
+    z.backward(g)
+    tz, tg = TOL[(dtype, d)]
+    if d == 3 and dtype == torch.float32:
+        tz, tg = 1e-3, 1e-2
+    yn, wn, gn = y.detach().double().cpu().numpy(), w.double().cpu().numpy(), g.double().cpu().numpy()
+    for b in sorted(set([0, B - 1, B // 2])):
+        lb = lam_np[:, b] if per_date else lam_np[b]
+        o = O1.forward_backward(yn[:, b], wn[:, b], lb, d, gn[:, b])
+        ez = np.max(np.abs(z[:, b].detach().double().cpu().numpy() - o["z"].astype(float)))
+        assert ez / ymax_observed(yn[:, b], wn[:, b]) <= tz, (case, b, ez)
+        assert rel_series(y.grad[:, b].double().cpu().numpy(), o["ybar"]).max() <= tg, (case, b)
+        if per_date:
+            assert rel_series(lam.grad[:, b].double().cpu().numpy(), o["lambar"]).max() <= tg, (case, b)
