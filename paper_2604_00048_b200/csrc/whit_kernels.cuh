@@ -129,6 +129,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 prefetch of a tensor box (no shared memory, no completion): the next tile's bytes start moving from
+// HBM one tile earlier than its shared-memory load, which then hits L2.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
@@ -300,6 +310,9 @@ template <int D> struct Ck {
 #ifndef WHIT_BWD_WARPS
 #define WHIT_BWD_WARPS 2
 #endif
+#ifndef WHIT_L2_PREFETCH
+#define WHIT_L2_PREFETCH 0
+#endif
 #ifndef WHIT_TILE_ST
 #define WHIT_TILE_ST 2
 #endif
@@ -352,6 +365,21 @@ __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage
   }
   if (BWD && !up) tma_load_3d(stage + L::OFF_DZ, &p.tm_dz, c0, t0, band, bar);
   if (LOSS && !up) tma_load_2d(stage + L::OFF_LW, &p.tm_lw, c0, t0, bar);
+#if WHIT_L2_PREFETCH
+  // the tile after this one (one more tile of HBM traffic in flight per warp, held in L2)
+  if (i + 1 < 2 * C) {
+    const bool up1 = i + 1 < C;
+    const int c1 = up1 ? i + 1 : 2 * C - 2 - i;
+    const int t1 = c1 * L::K;
+    tma_prefetch_3d(&p.tm_rhs, c0, t1, band);
+    if (!WB) tma_prefetch_2d(&p.tm_w, c0, t1);
+    if (PD) {
+      if (up1) tma_prefetch_2d(&p.tm_lam_up, c0, t1);
+      else tma_prefetch_2d(&p.tm_lam_dn, c0, t1 - D);
+    }
+    if (BWD && !up1) tma_prefetch_3d(&p.tm_dz, c0, t1, band);
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ per-thread sweep bodies
