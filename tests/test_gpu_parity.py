@@ -1010,3 +1010,20 @@ def test_randomised_shapes_through_autograd(case):
         assert rel_series(y.grad[:, b].double().cpu().numpy(), o["ybar"]).max() <= tg, (case, b)
         if per_date:
             assert rel_series(lam.grad[:, b].double().cpu().numpy(), o["lambar"]).max() <= tg, (case, b)
+
+
+def test_host_executor_bands_forward_only_f64():
+    """whit_run_host_bands without grad_z (forward only), fp64 planes, scalar lambda, ragged last chunk."""
+    import paper_2604_00048_b200 as P
+
+    d, C, T, B = 2, 3, 150, 202
+    x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, lam_mode="scalar", device="cuda",
+                                dtype=torch.float64, seed=82)
+    ws = P.Workspace(d, T, B, torch.float64, False, C=C)
+    z = torch.empty_like(x["y"])
+    P.whit_forward_bands(x["y"], x["w"], x["lam"], d, T, B, C, z, ws)
+    h = {k: x[k].cpu().pin_memory() for k in ("y", "w", "lam")}
+    hz = torch.empty_like(h["y"]).pin_memory()
+    P.whit_run_host_bands(h["y"], h["w"], h["lam"], None, d, hz, chunk=64, nbuf=2)
+    torch.cuda.synchronize()
+    assert torch.equal(hz, z.cpu())
