@@ -310,6 +310,9 @@ template <int D> struct Ck {
 #ifndef WHIT_BWD_WARPS
 #define WHIT_BWD_WARPS 2
 #endif
+#ifndef WHIT_IRR_UP_UNROLL
+#define WHIT_IRR_UP_UNROLL 8
+#endif
 #ifndef WHIT_L2_PREFETCH
 #define WHIT_L2_PREFETCH 0
 #endif
@@ -906,6 +909,7 @@ template <int D, typename IO, bool PD, bool BWD>
 __global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params p) {
   using L = IrrLayout<D, IO, PD, BWD>;
   constexpr int K = L::K, ST = L::ST, WARPS = L::WARPS;
+  constexpr int UP_UNROLL = WHIT_IRR_UP_UNROLL;
   constexpr int NFAC = Ck<D>::NFAC;
   constexpr int NW = Newton<IO>::N;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -964,7 +968,7 @@ __global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params 
 #pragma unroll
       for (int i = 0; i < D; ++i) ck[(long long)i * B] = S.f.v[i];
     }
-#pragma unroll
+#pragma unroll UP_UNROLL  // (state-only loop: not fully unrolled, smaller code)
     for (int k = 0; k < K; ++k) {
       const int t = t0 + k;
       if (t >= T) break;

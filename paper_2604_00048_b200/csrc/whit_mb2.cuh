@@ -74,6 +74,15 @@ struct MB2Layout {
 template <int D, typename IO, bool PD, bool BWD, bool IRR = false>
 __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_constant__ Params p) {
   using L = MB2Layout<D, IO, PD, BWD, IRR>;
+#ifndef WHIT_MB2_IRR_FUNROLL
+#define WHIT_MB2_IRR_FUNROLL 2
+#endif
+  // factor-warp row loops: the irregular grid's per-row stencil makes them long (instruction cache)
+  constexpr int FROW_UNROLL = IRR ? WHIT_MB2_IRR_FUNROLL : 8;
+#ifndef WHIT_MB2_IRR_BUNROLL
+#define WHIT_MB2_IRR_BUNROLL 8
+#endif
+  constexpr int BROW_UNROLL = IRR ? WHIT_MB2_IRR_BUNROLL : 8;  // band warps' up-sweep rows
   constexpr int K = L::K, ST = L::ST, FST = L::FST, NFAC = Ck<D>::NFAC, NW = Newton<IO>::N, BPW = L::BPW;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t f_full[FST];
@@ -183,7 +192,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       double* FMU = reinterpret_cast<double*>(F + L::FB_MU) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
       publish_pre_mu(FMU);
-#pragma unroll
+#pragma unroll FROW_UNROLL
       for (int k = 0; k < K; ++k) {
         const int t = t0 + k;
         const IO wio = t_w[k * 32];
@@ -269,7 +278,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       double* FC0 = reinterpret_cast<double*>(F + L::FB_C0) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
       publish_pre_mu(FMU);
-#pragma unroll
+#pragma unroll FROW_UNROLL
       for (int k = 0; k < K; ++k) {
         const int t = t0 + k;
         const IO wio = t_w[k * 32];
@@ -352,7 +361,7 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     auto up_rows = [&](auto tail_tag) {
       constexpr bool TAIL = decltype(tail_tag)::value;  // the chunk reaches row T: stop there
       const int n = T - t0;
-#pragma unroll
+#pragma unroll BROW_UNROLL
       for (int k = 0; k < K; ++k) {
         if (TAIL && k >= n) break;
         const IO wio = FW[k * 32];
