@@ -25,6 +25,7 @@
 #pragma once
 #include <cuda.h>
 #include <cstdint>
+#include <type_traits>
 
 namespace whit {
 
@@ -893,8 +894,9 @@ __device__ __forceinline__ void issue_tile_irr(const Params& p, unsigned char* s
 
 // mu and c0 of column k = t0 + kk (kk may be in [-D, K)), times tile row index kk + D.
 template <int D, typename IO, int NEWTON>
-__device__ __forceinline__ void tile_col(const IO* tt, int kk, int k, int T, double (&mu)[D], double& c0) {
-  if (k < 0 || k >= T - D) {
+__device__ __forceinline__ void tile_col(const IO* tt, int kk, int k, int T, double (&mu)[D], double& c0,
+                                         bool check = true) {
+  if (check && (k < 0 || k >= T - D)) {
     binomial_col<D>(mu);
     c0 = 0.0;
     return;
@@ -968,24 +970,31 @@ __global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params 
 #pragma unroll
       for (int i = 0; i < D; ++i) ck[(long long)i * B] = S.f.v[i];
     }
-#pragma unroll UP_UNROLL  // (state-only loop: not fully unrolled, smaller code)
-    for (int k = 0; k < K; ++k) {
-      const int t = t0 + k;
-      if (t >= T) break;
-      const IO wio = t_w[k * 32];
-      const double w = to_f64<IO>(wio);
-      double mu_t[D], c0;
-      tile_col<D, IO, NW>(t_tt, k, t, T, mu_t, c0);
-      const double lraw = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
-      const double lt = (t < TmD) ? lraw * c0 * c0 : 0.0;  // Lambda~_t = lambda_t c_{t,0}^2
-      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
-      double A[D], Dt, idt, vt;
-      ldl_step_irr<D, NW>(S, mu_t, w, lt, bb, A, Dt, idt, vt);
-      if (!BWD) {
-        nobs += (wio > IO(0));
-        allpos = allpos && (Dt > 0.0);
+    // EDGE: the chunk touches rows >= T - D (no difference row / past the end): per-row checks; interior
+    // chunks (the steady state) run without them
+    auto up_rows = [&](auto edge_tag) {
+      constexpr bool EDGE = decltype(edge_tag)::value;
+#pragma unroll UP_UNROLL
+      for (int k = 0; k < K; ++k) {
+        const int t = t0 + k;
+        if (EDGE && t >= T) break;
+        const IO wio = t_w[k * 32];
+        const double w = to_f64<IO>(wio);
+        double mu_t[D], c0;
+        tile_col<D, IO, NW>(t_tt, k, t, T, mu_t, c0, EDGE);
+        const double lraw = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
+        const double lt = (!EDGE || t < TmD) ? lraw * c0 * c0 : 0.0;  // Lambda~_t = lambda_t c_{t,0}^2
+        const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+        double A[D], Dt, idt, vt;
+        ldl_step_irr<D, NW>(S, mu_t, w, lt, bb, A, Dt, idt, vt);
+        if (!BWD) {
+          nobs += (wio > IO(0));
+          allpos = allpos && (Dt > 0.0);
+        }
       }
-    }
+    };
+    if (t0 + K > TmD) up_rows(std::true_type{});
+    else up_rows(std::false_type{});
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
@@ -1055,63 +1064,68 @@ __global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params 
       S.f.lm[i] = l;
       S.f.id[i] = (tj < 0) ? 1.0 : rcp64<NW>(l + S.f.dl[i]);
     }
-    double q[K], Ak[K][D], Mk[K][D], c0k[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int t = t0 + k;
-      const IO wio = t_w[k * 32];
-      const double w = to_f64<IO>(wio);
-      double c0;
-      tile_col<D, IO, NW>(t_tt, k, t, T, Mk[k], c0);
-      c0k[k] = c0;
-      const double lraw = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
-      const double lt = (t < TmD) ? lraw * c0 * c0 : 0.0;
-      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
-      double Dt, idt, vt;
-      ldl_step_irr<D, NW>(S, Mk[k], w, lt, bb, Ak[k], Dt, idt, vt);
-      q[k] = vt * idt;
-      if (t >= T) {
-        q[k] = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) Ak[k][j] = 0.0;
+    auto down_rows = [&](auto edge_tag) {
+      constexpr bool EDGE = decltype(edge_tag)::value;  // the chunk touches rows >= T - D
+      double q[K], Ak[K][D], Mk[K][D], c0k[K];
+  #pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int t = t0 + k;
+        const IO wio = t_w[k * 32];
+        const double w = to_f64<IO>(wio);
+        double c0;
+        tile_col<D, IO, NW>(t_tt, k, t, T, Mk[k], c0, EDGE);
+        c0k[k] = c0;
+        const double lraw = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
+        const double lt = (!EDGE || t < TmD) ? lraw * c0 * c0 : 0.0;
+        const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+        double Dt, idt, vt;
+        ldl_step_irr<D, NW>(S, Mk[k], w, lt, bb, Ak[k], Dt, idt, vt);
+        q[k] = vt * idt;
+        if (EDGE && t >= T) {
+          q[k] = 0.0;
+  #pragma unroll
+          for (int j = 0; j < D; ++j) Ak[k][j] = 0.0;
+        }
       }
-    }
-    if (lane == 0) bulk_wait_read0();
-    __syncwarp();
-#pragma unroll
-    for (int k = K - 1; k >= 0; --k) {
-      const int t = t0 + k;
-      double z = q[k];
-      // z_t = q_t - sum_j (M~[t+j][t] + A[t+j][j]) z_{t+j},  M~[t+j][t] = mu_t[j]
-#pragma unroll
-      for (int j = D; j >= 1; --j) {
-        const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
-        z = fma(-Mk[k][j - 1], zw[j - 1], z);
-        z = fma(-a, zw[j - 1], z);
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+  #pragma unroll
+      for (int k = K - 1; k >= 0; --k) {
+        const int t = t0 + k;
+        double z = q[k];
+        // z_t = q_t - sum_j (M~[t+j][t] + A[t+j][j]) z_{t+j},  M~[t+j][t] = mu_t[j]
+  #pragma unroll
+        for (int j = D; j >= 1; --j) {
+          const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
+          z = fma(-Mk[k][j - 1], zw[j - 1], z);
+          z = fma(-a, zw[j - 1], z);
+        }
+        // (D z)_t = c_{t,0} (z_t + sum_j mu_t[j] z_{t+j})
+        double u = z;
+  #pragma unroll
+        for (int j = 1; j <= D; ++j) u = fma(Mk[k][j - 1], zw[j - 1], u);
+        const double dz = c0k[k] * u;
+  #pragma unroll
+        for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
+        zw[0] = z;
+        if (!BWD) {
+          so0[k * 32 + lane] = from_f64<IO>(z);
+          so1[k * 32 + lane] = from_f64<IO>(dz);
+        } else {
+          const double w = to_f64<IO>(t_w[k * 32]);
+          so0[k * 32 + lane] = from_f64<IO>(w * z);
+          const double g = -dz * to_f64<IO>(t_dz[k * 32]);
+          if (PD) so1[k * 32 + lane] = from_f64<IO>(g);
+          else if (!EDGE || t < TmD) lam_acc += g;
+        }
       }
-      // (D z)_t = c_{t,0} (z_t + sum_j mu_t[j] z_{t+j})
-      double u = z;
-#pragma unroll
-      for (int j = 1; j <= D; ++j) u = fma(Mk[k][j - 1], zw[j - 1], u);
-      const double dz = c0k[k] * u;
-#pragma unroll
-      for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
-      zw[0] = z;
-      if (!BWD) {
-        so0[k * 32 + lane] = from_f64<IO>(z);
-        so1[k * 32 + lane] = from_f64<IO>(dz);
-      } else {
-        const double w = to_f64<IO>(t_w[k * 32]);
-        so0[k * 32 + lane] = from_f64<IO>(w * z);
-        const double g = -dz * to_f64<IO>(t_dz[k * 32]);
-        if (PD) so1[k * 32 + lane] = from_f64<IO>(g);
-        else if (t < TmD) lam_acc += g;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) { cA[i][j] = Ak[i][j]; cM[i][j] = Mk[i][j]; }
+  #pragma unroll
+      for (int i = 0; i < D; ++i)
+  #pragma unroll
+        for (int j = 0; j < D; ++j) { cA[i][j] = Ak[i][j]; cM[i][j] = Mk[i][j]; }
+    };
+    if (t0 + K > TmD) down_rows(std::true_type{});
+    else down_rows(std::false_type{});
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
