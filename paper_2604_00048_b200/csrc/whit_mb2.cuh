@@ -146,15 +146,16 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
     int it = 0, fb = 0;  // fb: factor-buffer sequence number
     // one factor row: daily grid (ldl_step, binomial stencil) or uneven dates (R-18: stencil of
     // column t from the dates tile, Lambda~_t = lambda_t c_{t,0}^2, ldl_step_irr)
+    // edge: the chunk touches rows >= T - d (range checks needed); interior chunks skip them
     auto factor_row = [&](const IO* t_tt, int k, int t, double w, double lraw, double (&A)[D], double& Dt,
-                          double& idt, double (&mu_t)[D], double& c0) {
+                          double& idt, double (&mu_t)[D], double& c0, bool edge) {
       double vt;
       if constexpr (IRR) {
-        tile_col<D, IO, NW>(t_tt, k, t, T, mu_t, c0);
-        const double lt = (t < TmD) ? lraw * c0 * c0 : 0.0;
+        tile_col<D, IO, NW>(t_tt, k, t, T, mu_t, c0, edge);
+        const double lt = (!edge || t < TmD) ? lraw * c0 * c0 : 0.0;
         ldl_step_irr<D, NW>(S, mu_t, w, lt, 0.0, A, Dt, idt, vt);
       } else {
-        const double lt = (t < TmD) ? lraw : 0.0;
+        const double lt = (!edge || t < TmD) ? lraw : 0.0;
         ldl_step<D, NW>(st, w, lt, 0.0, A, Dt, idt, vt);
       }
     };
@@ -192,26 +193,31 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       double* FMU = reinterpret_cast<double*>(F + L::FB_MU) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
       publish_pre_mu(FMU);
+      auto up_rows = [&](auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll FROW_UNROLL
-      for (int k = 0; k < K; ++k) {
-        const int t = t0 + k;
-        const IO wio = t_w[k * 32];
-        const double w = to_f64<IO>(wio);
-        const double lraw = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
-        double A[D], Dt, idt, mu_t[D], c0;
-        factor_row(t_tt, k, t, w, lraw, A, Dt, idt, mu_t, c0);
+        for (int k = 0; k < K; ++k) {
+          const int t = t0 + k;
+          const IO wio = t_w[k * 32];
+          const double w = to_f64<IO>(wio);
+          const double lraw = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
+          double A[D], Dt, idt, mu_t[D], c0;
+          factor_row(t_tt, k, t, w, lraw, A, Dt, idt, mu_t, c0, EDGE);
 #pragma unroll
-        for (int j = 0; j < D; ++j) FA[(k * D + j) * 32] = A[j];
-        if constexpr (IRR) {
+          for (int j = 0; j < D; ++j) FA[(k * D + j) * 32] = A[j];
+          if constexpr (IRR) {
 #pragma unroll
-          for (int j = 0; j < D; ++j) FMU[((k + D) * D + j) * 32] = mu_t[j];
+            for (int j = 0; j < D; ++j) FMU[((k + D) * D + j) * 32] = mu_t[j];
+          }
+          FW[k * 32] = wio;
+          if (!BWD && (!EDGE || t < T)) {
+            nobs += (wio > IO(0));
+            allpos = allpos && (Dt > 0.0);
+          }
         }
-        FW[k * 32] = wio;
-        if (!BWD && t < T) {
-          nobs += (wio > IO(0));
-          allpos = allpos && (Dt > 0.0);
-        }
-      }
+      };
+      if (t0 + K > TmD) up_rows(std::true_type{});
+      else up_rows(std::false_type{});
       __syncwarp();
       if (lane == 0) mbar_arrive(&fac_full[fb % L::NFB]);  // release: this warp's smem writes
       if (lane == 0 && it + FST < ntiles) {
@@ -278,25 +284,30 @@ __global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_consta
       double* FC0 = reinterpret_cast<double*>(F + L::FB_C0) + lane;
       IO* FW = reinterpret_cast<IO*>(F + L::FB_W) + lane;
       publish_pre_mu(FMU);
+      auto down_rows = [&](auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll FROW_UNROLL
-      for (int k = 0; k < K; ++k) {
-        const int t = t0 + k;
-        const IO wio = t_w[k * 32];
-        const double w = to_f64<IO>(wio);
-        const double lraw = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
-        double A[D], Dt, idt, mu_t[D], c0;
-        factor_row(t_tt, k, t, w, lraw, A, Dt, idt, mu_t, c0);
-        const bool past = t >= T;  // rows past the end: z = 0 (q = 0, A = 0)
+        for (int k = 0; k < K; ++k) {
+          const int t = t0 + k;
+          const IO wio = t_w[k * 32];
+          const double w = to_f64<IO>(wio);
+          const double lraw = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
+          double A[D], Dt, idt, mu_t[D], c0;
+          factor_row(t_tt, k, t, w, lraw, A, Dt, idt, mu_t, c0, EDGE);
+          const bool past = EDGE && t >= T;  // rows past the end: z = 0 (q = 0, A = 0)
 #pragma unroll
-        for (int j = 0; j < D; ++j) FA[(k * D + j) * 32] = past ? 0.0 : A[j];
-        FI[k * 32] = past ? 0.0 : idt + poison;
-        if constexpr (IRR) {
+          for (int j = 0; j < D; ++j) FA[(k * D + j) * 32] = past ? 0.0 : A[j];
+          FI[k * 32] = past ? 0.0 : idt + poison;
+          if constexpr (IRR) {
 #pragma unroll
-          for (int j = 0; j < D; ++j) FMU[((k + D) * D + j) * 32] = mu_t[j];
-          FC0[k * 32] = c0;
+            for (int j = 0; j < D; ++j) FMU[((k + D) * D + j) * 32] = mu_t[j];
+            FC0[k * 32] = c0;
+          }
+          FW[k * 32] = wio;
         }
-        FW[k * 32] = wio;
-      }
+      };
+      if (t0 + K > TmD) down_rows(std::true_type{});
+      else down_rows(std::false_type{});
       __syncwarp();
       if (lane == 0) mbar_arrive(&fac_full[fb % L::NFB]);
       if (lane == 0 && it + FST < ntiles) {
