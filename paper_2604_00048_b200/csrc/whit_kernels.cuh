@@ -1231,18 +1231,23 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
 #pragma unroll
         for (int k = 0; k < D - 1 - m; ++k) ck[(long long)(f++) * B] = st.ap[m][k];
     }
+    auto up_rows = [&](auto edge_tag) {  // EDGE: the chunk touches rows >= T - d
+      constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll 4
-    for (int k = 0; k < K; ++k) {
-      const int t = t0 + k;
-      if (t >= T) break;
-      const IO wio = t_w[k * 32];
-      const double w = to_f64<IO>(wio);
-      const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : (t < TmD ? lam_s : 0.0);
-      double A[D], Dt, idt, vt;
-      ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, A, Dt, idt, vt);
-      nobs += (wio > IO(0));
-      allpos = allpos && (Dt > 0.0);
-    }
+      for (int k = 0; k < K; ++k) {
+        const int t = t0 + k;
+        if (EDGE && t >= T) break;
+        const IO wio = t_w[k * 32];
+        const double w = to_f64<IO>(wio);
+        const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : ((!EDGE || t < TmD) ? lam_s : 0.0);
+        double A[D], Dt, idt, vt;
+        ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, A, Dt, idt, vt);
+        nobs += (wio > IO(0));
+        allpos = allpos && (Dt > 0.0);
+      }
+    };
+    if (t0 + K > TmD) up_rows(std::true_type{});
+    else up_rows(std::false_type{});
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
@@ -1284,7 +1289,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
     const IO* t_w = reinterpret_cast<const IO*>(stg + V::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + V::OFF_LAM) + lane;  // row k <-> t0 - D + k
     const int t0 = c * K;
-    const bool ragged = (t0 + K > T);
+    const bool ragged = (t0 + K > T), edge = (t0 + K > TmD);
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       const int tj = t0 - 1 - i;
@@ -1300,7 +1305,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
       const int t = t0 + k;
       const double w = to_f64<IO>(t_w[k * 32]);
       double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
-      if (!PD) lt = (t < TmD) ? lt : 0.0;
+      if (!PD) lt = (!edge || t < TmD) ? lt : 0.0;
       double Dt, vt;
       ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, Ak[k], Dt, idk[k], vt);
       if (ragged && t >= T) {  // rows past the end: Sigma = 0 there, no coupling
