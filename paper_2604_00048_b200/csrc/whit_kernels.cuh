@@ -859,7 +859,8 @@ __device__ __forceinline__ void ldl_step_irr(IState<D>& S, const double (&mu_t)[
 // Stage: rhs K rows, w K rows, times K+2D rows (t0-D .. t0+K+D-1), lambda (K / K+D rows), D z K rows.
 template <int D, typename IO, bool PD, bool BWD>
 struct IrrLayout {
-  static constexpr int K = 8, ST = 2, WARPS = 4;
+  // d = 3 holds a 3 x 3 stencil window per row: more registers, so 2-warp CTAs at <= 224 registers
+  static constexpr int K = 8, ST = 2, WARPS = D == 3 ? 2 : 4;  // (the kernel caps d = 3 at 224 registers)
   static constexpr int ROW = 32 * (int)sizeof(IO);
   static constexpr int OFF_RHS = 0;
   static constexpr int OFF_W = K * ROW;
@@ -908,7 +909,7 @@ __device__ __forceinline__ void tile_col(const IO* tt, int kk, int k, int T, dou
 }
 
 template <int D, typename IO, bool PD, bool BWD>
-__global__ void __maxnreg__(168) whit_irr_kernel(const __grid_constant__ Params p) {
+__global__ void __maxnreg__((D == 3 ? 224 : 168)) whit_irr_kernel(const __grid_constant__ Params p) {
   using L = IrrLayout<D, IO, PD, BWD>;
   constexpr int K = L::K, ST = L::ST, WARPS = L::WARPS;
   constexpr int UP_UNROLL = WHIT_IRR_UP_UNROLL;
