@@ -68,11 +68,14 @@ struct MB2Layout {
   }
 };
 
+#ifndef WHIT_MB2_MAXREG_D3
+#define WHIT_MB2_MAXREG_D3 168
+#endif
 #ifndef WHIT_MB2_MAXREG
 #define WHIT_MB2_MAXREG 168
 #endif
 template <int D, typename IO, bool PD, bool BWD, bool IRR = false>
-__global__ void __maxnreg__(WHIT_MB2_MAXREG) whit_mb2_kernel(const __grid_constant__ Params p) {
+__global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whit_mb2_kernel(const __grid_constant__ Params p) {
   using L = MB2Layout<D, IO, PD, BWD, IRR>;
 #ifndef WHIT_MB2_IRR_FUNROLL
 #define WHIT_MB2_IRR_FUNROLL 2

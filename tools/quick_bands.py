@@ -7,8 +7,8 @@ import synth
 
 C = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 131072
-d = 2
-x = synth.make_inputs_bands("hetero", C, B=B, device="cuda")
+d = int(os.environ.get("QB_D", "2"))
+x = synth.make_inputs_bands("hetero", C, B=B, d=d, device="cuda")
 x.pop("lam_mode", None)
 y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
 _, T, _ = y.shape
