@@ -1,21 +1,24 @@
 // libwhit multi-band kernel with a shared factor warp (NEXT-1, P:28 / P:147: the C bands of a
 // pixel share W and Lambda, hence Omega and its factor).
 //
-// CTA = ceil(C/2) band warps (two bands each) + 1 factor warp over 32 pixels:
-//  * the factor warp streams w and lambda (its own TMA ring), runs the deviation-form LDL^T
-//    (ldl_step, R-10) once per pixel and publishes, per K-row chunk, the rows
-//    (A_{t,1..d}, 1/D_t, w_t) into a ring of NFB (3-4) shared-memory factor buffers (mbarriers
-//    fac_full / fac_empty); it writes the factor checkpoints and, in the down sweep, recomputes
-//    each chunk's factor from them;
-//  * each band warp streams its two bands' right-hand sides (TMA) and runs the 4-flop
-//    forward-substitution recurrences and the back substitutions with the published rows (two
-//    independent chains per lane = ILP), storing z / D z / grad_y straight to HBM with coalesced
-//    128-B warp stores (no staging), reading D z in the backward with plain loads issued a chunk
-//    ahead of use.  Shared memory per CTA (~105-113 KB at C = 10, fp32) lets two CTAs -- two
-//    independent pixel groups and factor chains -- share an SM.
-// The band warps execute exactly the fp64 operation sequence of the single-band kernel, so every
-// band's z and grad_y equal the independent-series results bit for bit; grad_lambda is the band
-// sum in fp64 (fixed order), reduced in shared memory.
+// CTA = ceil(C/2) band warps (two bands each) + 1 factor warp over 32 pixels, K = 8-row chunks:
+//  * the factor warp streams w and lambda (and, IRR, the acquisition dates) through its own TMA ring
+//    (4 slots in the forward, 2 in the backward), runs the deviation-form LDL^T (ldl_step, R-10; IRR:
+//    ldl_step_irr on the per-row dspline stencils, R-18) once per pixel and publishes, per chunk, the
+//    rows (A_{t,1..d}, 1/D_t, w_t; IRR also mu and c_{t,0}) into a ring of 3 shared-memory factor buffers
+//    (mbarriers fac_full / fac_empty); it writes the factor checkpoints and, in the down sweep,
+//    recomputes each chunk's factor from them (loaded a chunk ahead);
+//  * each band warp streams its two bands' right-hand sides (TMA) and runs the forward-substitution
+//    recurrences and the back substitutions with the published rows (two independent chains per lane =
+//    ILP), storing z / D z / grad_y straight to HBM with coalesced 128-B warp stores (no staging),
+//    reading D z in the backward with plain loads issued a chunk ahead of use; per-date dL/dlambda
+//    partials are summed across the band warps through shared memory (one barrier per chunk).
+//  * interior chunks run without per-row range checks (compile-time interior / edge split).
+// Shared memory per CTA (~54-67 KB at C = 10, fp32) and <= 168 registers give two CTAs -- two
+// independent pixel groups and factor chains -- per SM at C = 10, four at C <= 4.
+// The band warps execute exactly the fp64 operation sequence of the single-band kernels, so every
+// band's z and grad_y equal the independent-series results bit for bit; grad_lambda is the band sum
+// in fp64 (fixed order).
 #pragma once
 #include <type_traits>
 #include "whit_kernels.cuh"
