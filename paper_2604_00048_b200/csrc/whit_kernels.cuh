@@ -58,10 +58,10 @@ struct Params {
   CUtensorMap tm_out1;    // forward: D z cache [nb][T-d][B] (3-D); backward: per-date grad_lambda [T-d][B] (2-D)
   const void* lam_scalar; // [B] (scalar lambda mode)
   const void* lam_plane;  // [T-d][B] (per-date mode; read directly only by the cold failure path)
-  void* out0;             // backward: grad_y [T][B] (direct stores); multi-band: z / grad_y [nb][T][B]
+  void* out0;             // multi-band kernel (direct stores): z (forward) / grad_y (backward) [nb][T][B]
   const void* dz_cache;   // multi-band backward: the forward's D z cache [nb][T-d][B]
-  void* out1;             // backward: grad_lambda, [T-d][B] per date (direct stores) or [B] scalar
-  CUtensorMap tm_lw;      // LOSS: loss weights [T][B], box {32, K}
+  void* out1;             // multi-band forward: D z cache; backward: grad_lambda [T-d][B] per date or [B] scalar
+  CUtensorMap tm_lw;      // LOSS: loss weights [T][B], box {32, K}; irregular grid: the dates [T][B], box {32, K+2d}
   CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
   void* loss;             // LOSS: per-series loss [B]
   const uint32_t* wbits;  // WB: bit-packed 0/1 weights [ceil(T/32)][B], bit t%32 of word t/32
