@@ -659,6 +659,7 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
   if ((st = encode_map(&p.tm_lw, loss_w, ws->dt, B, T, kK)) != WHIT_OK) return st;
   if ((st = encode_map(&p.tm_out2, grad_z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
   p.loss = loss;
+  p.out2 = grad_z;
   ws->have_fwd = false;
   const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
   if (ws->dt == WHIT_F32)

@@ -64,6 +64,7 @@ struct Params {
   CUtensorMap tm_lw;      // LOSS: loss weights [T][B], box {32, K}; irregular grid: the dates [T][B], box {32, K+2d}
   CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
   void* loss;             // LOSS: per-series loss [B]
+  void* out2;             // LOSS: grad_z = dL/dz [T][B] (direct coalesced stores)
   const uint32_t* wbits;  // WB: bit-packed 0/1 weights [ceil(T/32)][B], bit t%32 of word t/32
   double* ck_fac;         // factor checkpoints [C][NFAC][B] (forward up sweep; read by every later sweep)
   double* ck_rhs_f;       // forward rhs checkpoints [C][nb][d][B]
@@ -335,7 +336,9 @@ template <typename IO, int D, bool BWD> struct Tile {
 constexpr int kMaxBands = 10;
 
 template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false> struct Layout {
-  static constexpr int K = Tile<IO, D, BWD>::K, ST = Tile<IO, D, BWD>::ST, WARPS = Tile<IO, D, BWD>::WARPS;
+  // LOSS: 2-warp CTAs (its stage carries the loss weights too: 10 warps/SM fit at <= 200 registers)
+  static constexpr int K = Tile<IO, D, BWD>::K, ST = Tile<IO, D, BWD>::ST,
+                       WARPS = LOSS ? 2 : Tile<IO, D, BWD>::WARPS;
   static constexpr int ROW = 32 * (int)sizeof(IO);  // bytes of one staged time row (one warp)
   static constexpr int OFF_RHS = 0;
   static constexpr int OFF_W = K * ROW;                        // (absent with WB: w comes as bits)
@@ -346,7 +349,7 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
   // outputs are staged per chunk and written by TMA tensor stores (staging in the consumed input slots,
   // and direct 128-B warp stores, were measured no faster: DESIGN.md §5)
-  static constexpr int WARP_SMEM = ST * STAGE + (LOSS ? 3 : 2) * OUT;
+  static constexpr int WARP_SMEM = ST * STAGE + 2 * OUT;  // (LOSS: grad_z goes out with direct stores)
   static constexpr int SMEM = WARPS * WARP_SMEM;
   static constexpr uint32_t BYTES_UP = ((WB ? 1 : 2) * K + (PD ? K : 0)) * ROW;
   static constexpr uint32_t BYTES_DN = ((WB ? 1 : 2) * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
@@ -481,7 +484,8 @@ struct Sweep {
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
-                                                    double two_over_T = 0.0, uint32_t wm = 0) {
+                                                    double two_over_T = 0.0, uint32_t wm = 0, IO* gz0 = nullptr,
+                                                    long long Bst = 0, bool valid = false) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -532,7 +536,7 @@ struct Sweep {
           const IO yr = reinterpret_cast<const IO*>(stg + L::OFF_RHS)[lane + k * 32];
           const double e = (lw != IO(0)) ? z - to_f64<IO>(yr) : 0.0;  // unscored dates: exactly 0 (y may be NaN)
           const double lwe = to_f64<IO>(lw) * e;
-          so2[k * 32] = from_f64<IO>(two_over_T * lwe);
+          if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = from_f64<IO>(two_over_T * lwe);
           if (!RAGGED || t < T) lam_acc = fma(lwe, e, lam_acc);  // (forward: lam_acc holds the loss sum)
         }
       } else {
@@ -586,7 +590,6 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   unsigned char* ring = smem + warp * L::WARP_SMEM;
   IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);             // output staging
   IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
-  IO* so2 = reinterpret_cast<IO*>(ring + ST * L::STAGE + 2 * L::OUT);  // LOSS only
   uint64_t* bars = full_bar[warp];
   const int ntiles = 2 * C;
 
@@ -728,18 +731,18 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
     if (lane == 0) bulk_wait_read0();
     __syncwarp();
     const double two_over_T = 2.0 / (double)T;
+    IO* const gz0 = LOSS ? reinterpret_cast<IO*>(p.out2) + (long long)t0 * B + b : nullptr;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    so2 + lane, two_over_T, wm);
+                                    nullptr, two_over_T, wm, gz0, B, valid);
     else
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   so2 + lane, two_over_T, wm);
+                                   nullptr, two_over_T, wm, gz0, B, valid);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
     if (lane == 0) {
       tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
       if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
-      if (LOSS) tma_store_3d(&p.tm_out2, so2, (int)bw, t0, 0);
       if (BWD && PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
       bulk_commit();
     }
