@@ -318,6 +318,9 @@ template <int D> struct Ck {
 #ifndef WHIT_L2_PREFETCH
 #define WHIT_L2_PREFETCH 0
 #endif
+#ifndef WHIT_BWD_DIRECT
+#define WHIT_BWD_DIRECT 1
+#endif
 #ifndef WHIT_TILE_ST
 #define WHIT_TILE_ST 2
 #endif
@@ -349,7 +352,10 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   static constexpr int OUT = K * ROW;                        // one staged output plane (TMA store)
   // outputs are staged per chunk and written by TMA tensor stores (staging in the consumed input slots,
   // and direct 128-B warp stores, were measured no faster: DESIGN.md §5)
-  static constexpr int WARP_SMEM = ST * STAGE + 2 * OUT;  // (LOSS: grad_z goes out with direct stores)
+  // backward outputs by direct coalesced stores (WHIT_BWD_DIRECT): no staging planes, 10 warps/SM
+  // (measured +2% backward on homo/hetero; the bit-W backward stays staged: direct was 8% slower there)
+  static constexpr bool BDIRECT = BWD && !WB && WHIT_BWD_DIRECT;
+  static constexpr int WARP_SMEM = ST * STAGE + (BDIRECT ? 0 : 2 * OUT);  // (LOSS: grad_z goes out directly)
   static constexpr int SMEM = WARPS * WARP_SMEM;
   static constexpr uint32_t BYTES_UP = ((WB ? 1 : 2) * K + (PD ? K : 0)) * ROW;
   static constexpr uint32_t BYTES_DN = ((WB ? 1 : 2) * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
@@ -485,7 +491,7 @@ struct Sweep {
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
                                                     double two_over_T = 0.0, uint32_t wm = 0, IO* gz0 = nullptr,
-                                                    long long Bst = 0, bool valid = false) {
+                                                    long long Bst = 0, bool valid = false, IO* gl0 = nullptr) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -552,8 +558,13 @@ struct Sweep {
           if (PD) gl = from_f64<IO>(g);
           else if (!RAGGED || t < TmD) lam_acc += g;
         }
-        so0[k * 32] = gy;
-        if (PD) so1[k * 32] = gl;
+        if (L::BDIRECT) {  // gz0: grad_y rows, gl0: grad_lambda rows of this chunk
+          if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = gy;
+          if (PD && valid && (!RAGGED || t < TmD)) gl0[(long long)k * Bst] = gl;
+        } else {
+          so0[k * 32] = gy;
+          if (PD) so1[k * 32] = gl;
+        }
       }
     }
 #pragma unroll
@@ -728,19 +739,23 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
     if (c > 0) WHIT_LOAD_CK(c - 1);
 
     // the staging tiles must have been read by the previous chunk's TMA stores
-    if (lane == 0) bulk_wait_read0();
-    __syncwarp();
+    if (!L::BDIRECT) {
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+    }
     const double two_over_T = 2.0 / (double)T;
-    IO* const gz0 = LOSS ? reinterpret_cast<IO*>(p.out2) + (long long)t0 * B + b : nullptr;
+    IO* const gz0 = LOSS ? reinterpret_cast<IO*>(p.out2) + (long long)t0 * B + b
+                  : L::BDIRECT ? reinterpret_cast<IO*>(p.out0) + (long long)t0 * B + b : nullptr;
+    IO* const gl0 = (L::BDIRECT && PD) ? reinterpret_cast<IO*>(p.out1) + (long long)t0 * B + b : nullptr;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    nullptr, two_over_T, wm, gz0, B, valid);
+                                    nullptr, two_over_T, wm, gz0, B, valid, gl0);
     else
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   nullptr, two_over_T, wm, gz0, B, valid);
+                                   nullptr, two_over_T, wm, gz0, B, valid, gl0);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && !L::BDIRECT) {
       tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
       if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
       if (BWD && PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);

@@ -11,9 +11,12 @@ import synth
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 3288
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 262144
-x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda")
+x = synth.make_inputs(os.environ.get("QD_W", "hetero"), B=B, T=T, d=d, device="cuda")
 y, w, lam, g = x["y"], x["w"], x["lam"], x["g"]
-ws = P.Workspace(d, T, B, torch.float32, True)
+ws = P.Workspace(d, T, B, torch.float32, lam.dim() == 2)
+if os.environ.get("QD_WBITS"):  # forward with the bit-packed W (the backward then reads the bits too)
+    bits = P.whit_pack_mask(w)
+    P.whit_forward = lambda y, w, *a: P.whit_forward_wbits(y, bits, *a)
 z, gy, gl = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam)
 for _ in range(3):
     P.whit_forward(y, w, lam, d, T, B, z, ws)
