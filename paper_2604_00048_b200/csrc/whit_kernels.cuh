@@ -321,6 +321,9 @@ template <int D> struct Ck {
 #ifndef WHIT_BWD_DIRECT
 #define WHIT_BWD_DIRECT 1
 #endif
+#ifndef WHIT_FWD_DIRECT  // plain forward by direct stores: measured neutral (hetero fwd 5.52-5.56 ms vs 5.51-5.55
+#define WHIT_FWD_DIRECT 0  // staged; the forward is register-limited to 12 warps/SM either way), so TMA stores stay
+#endif
 #ifndef WHIT_TILE_ST
 #define WHIT_TILE_ST 2
 #endif
@@ -355,7 +358,10 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   // backward outputs by direct coalesced stores (WHIT_BWD_DIRECT): no staging planes, 10 warps/SM
   // (measured +2% backward on homo/hetero; the bit-W backward stays staged: direct was 8% slower there)
   static constexpr bool BDIRECT = BWD && !WB && WHIT_BWD_DIRECT;
-  static constexpr int WARP_SMEM = ST * STAGE + (BDIRECT ? 0 : 2 * OUT);  // (LOSS: grad_z goes out directly)
+  // plain forward: z and D z by direct coalesced stores too (WHIT_FWD_DIRECT)
+  static constexpr bool FDIRECT = !BWD && !WB && !LOSS && WHIT_FWD_DIRECT;
+  static constexpr bool DIRECT = BDIRECT || FDIRECT;
+  static constexpr int WARP_SMEM = ST * STAGE + (DIRECT ? 0 : 2 * OUT);  // (LOSS: grad_z goes out directly)
   static constexpr int SMEM = WARPS * WARP_SMEM;
   static constexpr uint32_t BYTES_UP = ((WB ? 1 : 2) * K + (PD ? K : 0)) * ROW;
   static constexpr uint32_t BYTES_DN = ((WB ? 1 : 2) * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
@@ -535,8 +541,13 @@ struct Sweep {
       for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
       zw[0] = z;
       if (!BWD) {
-        so0[k * 32] = from_f64<IO>(z);
-        so1[k * 32] = from_f64<IO>(dz);
+        if (L::FDIRECT) {  // gz0: z rows, gl0: D z rows of this chunk
+          if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = from_f64<IO>(z);
+          if (valid && (!RAGGED || t < T - D)) gl0[(long long)k * Bst] = from_f64<IO>(dz);
+        } else {
+          so0[k * 32] = from_f64<IO>(z);
+          so1[k * 32] = from_f64<IO>(dz);
+        }
         if (LOSS) {  // masked MSE: L += lw (z - y)^2 / T, g = 2 lw (z - y) / T
           const IO lw = reinterpret_cast<const IO*>(stg + L::OFF_LW)[lane + k * 32];
           const IO yr = reinterpret_cast<const IO*>(stg + L::OFF_RHS)[lane + k * 32];
@@ -739,14 +750,15 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
     if (c > 0) WHIT_LOAD_CK(c - 1);
 
     // the staging tiles must have been read by the previous chunk's TMA stores
-    if (!L::BDIRECT) {
+    if (!L::DIRECT) {
       if (lane == 0) bulk_wait_read0();
       __syncwarp();
     }
     const double two_over_T = 2.0 / (double)T;
     IO* const gz0 = LOSS ? reinterpret_cast<IO*>(p.out2) + (long long)t0 * B + b
-                  : L::BDIRECT ? reinterpret_cast<IO*>(p.out0) + (long long)t0 * B + b : nullptr;
-    IO* const gl0 = (L::BDIRECT && PD) ? reinterpret_cast<IO*>(p.out1) + (long long)t0 * B + b : nullptr;
+                  : L::DIRECT ? reinterpret_cast<IO*>(p.out0) + (long long)t0 * B + b : nullptr;
+    IO* const gl0 = ((L::BDIRECT && PD) || L::FDIRECT) ? reinterpret_cast<IO*>(p.out1) + (long long)t0 * B + b
+                                                       : nullptr;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
                                     nullptr, two_over_T, wm, gz0, B, valid, gl0);
@@ -755,7 +767,7 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
                                    nullptr, two_over_T, wm, gz0, B, valid, gl0);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
-    if (lane == 0 && !L::BDIRECT) {
+    if (lane == 0 && !L::DIRECT) {
       tma_store_3d(&p.tm_out0, so0, (int)bw, t0, band);
       if (!BWD) tma_store_3d(&p.tm_out1, so1, (int)bw, t0, band);
       if (BWD && PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t0);
