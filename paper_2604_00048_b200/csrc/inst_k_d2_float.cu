@@ -1,0 +1,13 @@
+// Explicit instantiations: single-series daily-grid kernels, d = 2, float I/O (see whit_launch.cuh).
+#define WHIT_LAUNCH_DEFS
+#include "whit_launch.cuh"
+namespace whit_detail {
+#define WHIT_INST(PD)                                                                        \
+  template whit_status launch<2, float, PD, false, false, false>(const whit::Params&, cudaStream_t); \
+  template whit_status launch<2, float, PD, true, false, false>(const whit::Params&, cudaStream_t);  \
+  template whit_status launch<2, float, PD, false, true, false>(const whit::Params&, cudaStream_t);  \
+  template whit_status launch<2, float, PD, false, false, true>(const whit::Params&, cudaStream_t);  \
+  template whit_status launch<2, float, PD, true, false, true>(const whit::Params&, cudaStream_t);
+WHIT_INST(true)
+WHIT_INST(false)
+}  // namespace whit_detail

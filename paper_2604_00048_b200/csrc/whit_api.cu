@@ -15,12 +15,9 @@
 #include <mutex>
 #include <string>
 
-#include "whit_kernels.cuh"
-#include "whit_mb2.cuh"
+#include "whit_launch.cuh"
 
 using whit::Params;
-
-#include "whit_internal.h"
 
 namespace {
 thread_local std::string g_err;
@@ -159,8 +156,11 @@ struct DeviceGuard {
   }
 };
 
-// Dynamic smem budget of one CTA (227 KB opt-in minus the kernel's static barriers).
-constexpr int kSmemBudget = 232448 - 2048;
+using whit_detail::kSmemBudget;
+using whit_detail::launch;
+using whit_detail::launch_irr;
+using whit_detail::launch_mb2;
+using whit_detail::launch_var;
 
 // Largest band count whose shared-factor CTA (whit_mb2_kernel) fits shared memory, for every
 // (d, lambda mode, direction) of this dtype.
@@ -191,55 +191,6 @@ constexpr int max_bands_io() {
 static_assert(max_bands_io<float>() == whit::kMaxBands && max_bands_io<double>() == whit::kMaxBands,
               "every multi-band kernel fits kMaxBands bands in one CTA");
 int max_bands(whit_dtype dt) { return dt == WHIT_F32 ? max_bands_io<float>() : max_bands_io<double>(); }
-
-template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
-whit_status launch(const Params& p, cudaStream_t s) {
-  using L = whit::Layout<D, IO, PD, BWD, LOSS, WB>;
-  constexpr int max_smem = L::SMEM;
-  static_assert(max_smem <= kSmemBudget, "CTA shared memory over budget");
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, LOSS, WB>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    attr_err = cudaFuncSetAttribute(whit::whit_kernel<D, IO, PD, BWD, LOSS, WB>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-  });
-  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  // one series per thread, one TMA pipeline per warp
-  const int threads = 32 * L::WARPS;
-  const long long grid = (p.B + threads - 1) / threads;
-  whit::whit_kernel<D, IO, PD, BWD, LOSS, WB><<<dim3((unsigned)grid), dim3(threads), L::SMEM, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-  return WHIT_OK;
-}
-
-// Multi-band with a shared factor warp (NEXT-1): CTA = nb band warps + 1 factor warp (IRR: on
-// uneven acquisition dates, NEXT-2).
-template <int D, typename IO, bool PD, bool BWD, bool IRR = false>
-whit_status launch_mb2(const Params& p, cudaStream_t s) {
-  using L = whit::MB2Layout<D, IO, PD, BWD, IRR>;
-  constexpr int max_smem = L::smem(whit::kMaxBands);
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD, IRR>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    attr_err = cudaFuncSetAttribute(whit::whit_mb2_kernel<D, IO, PD, BWD, IRR>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    max_smem < kSmemBudget ? max_smem : kSmemBudget);
-  });
-  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  const int smem = L::smem(p.nb);
-  if (smem > kSmemBudget) return fail(WHIT_ERR_SHAPE, "%d bands need %d B of shared memory", p.nb, smem);
-  const long long grid = (p.B + 31) / 32;
-  const int threads = 32 * (L::nwarps(p.nb) + 1);
-  whit::whit_mb2_kernel<D, IO, PD, BWD, IRR><<<dim3((unsigned)grid), dim3(threads), smem, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-  return WHIT_OK;
-}
 
 template <typename IO, bool PD, bool BWD, bool MB>
 whit_status dispatch_d(int d, const Params& p, cudaStream_t s) {
@@ -302,26 +253,6 @@ whit_status dispatch_loss_d(int d, const Params& p, cudaStream_t s) {
   return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
 }
 
-template <int D, typename IO, bool PD>
-whit_status launch_var(const Params& p, cudaStream_t s) {
-  using V = whit::VarLayout<D, IO, PD>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(whit::whit_var_kernel<D, IO, PD>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    attr_err = cudaFuncSetAttribute(whit::whit_var_kernel<D, IO, PD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    V::SMEM);
-  });
-  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  const long long per_cta = 32 * V::WARPS;
-  const long long grid = (p.B + per_cta - 1) / per_cta;
-  whit::whit_var_kernel<D, IO, PD><<<dim3((unsigned)grid), dim3((unsigned)per_cta), V::SMEM, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-  return WHIT_OK;
-}
-
 template <typename IO, bool PD>
 whit_status dispatch_var_d(int d, const Params& p, cudaStream_t s) {
   switch (d) {
@@ -355,27 +286,6 @@ whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const voi
   p->T = int(ws->T);
   p->C = int((ws->T + kK - 1) / kK);
   p->nb = ws->nb;
-  return WHIT_OK;
-}
-
-// Irregular grid: maps with the IrrLayout tile heights (K = 8) and the times map (box K + 2d).
-template <int D, typename IO, bool PD, bool BWD>
-whit_status launch_irr(const Params& p, cudaStream_t s) {
-  using L = whit::IrrLayout<D, IO, PD, BWD>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(whit::whit_irr_kernel<D, IO, PD, BWD>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         (int)cudaSharedmemCarveoutMaxShared);
-    attr_err = cudaFuncSetAttribute(whit::whit_irr_kernel<D, IO, PD, BWD>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-  });
-  if (attr_err != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
-  const long long per_cta = 32 * L::WARPS;
-  const long long grid = (p.B + per_cta - 1) / per_cta;
-  whit::whit_irr_kernel<D, IO, PD, BWD><<<dim3((unsigned)grid), dim3((unsigned)per_cta), L::SMEM, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return WHIT_OK;
 }
 

@@ -1443,7 +1443,7 @@ __global__ void grad_w_kernel(const IO* __restrict__ w, const IO* __restrict__ y
 }
 
 // Count of failed series (info != 0) for whit_failures.
-__global__ void count_failures(const int32_t* __restrict__ info, long long B, unsigned long long* out) {
+static __global__ void count_failures(const int32_t* __restrict__ info, long long B, unsigned long long* out) {
   unsigned long long n = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < B; i += (long long)gridDim.x * blockDim.x)
     n += (info[i] != 0);
