@@ -73,23 +73,29 @@ class WhittakerFn(torch.autograd.Function):
             ws = L.Workspace(d, T, Bp, y.dtype, per_date, device=y.device)
             L.whit_forward(yp, wp, lp, d, T, Bp, z, ws)
             keep = (wp, lp, z)
-        ctx.ws, ctx.keep, ctx.B, ctx.Bp = ws, keep, B, Bp
-        ctx.yp = yp if ctx.needs_input_grad[1] else None  # dL/dw needs y (whit_grad_w)
+        # tensors go through save_for_backward (no z -> grad_fn -> ctx -> z reference cycle keeping the
+        # workspace alive, and autograd's version check guards w, lambda and z against in-place edits
+        # before the backward the ABI requires them for); only the host handle is a ctx attribute
+        need_w = ctx.needs_input_grad[1]
+        ctx.save_for_backward(*keep, yp if need_w else None)
+        ctx.ws, ctx.B, ctx.Bp, ctx.need_w = ws, B, Bp, need_w
         return z[..., :B] if Bp != B else z
 
     @staticmethod
     def backward(ctx, gz):
-        ws, keep = ctx.ws, ctx.keep
-        lp, z = keep[1], keep[2]
+        ws = ctx.ws
+        saved = ctx.saved_tensors
+        wp, lp, z = saved[0], saved[1], saved[2]
+        yp = saved[-1]
         gzp = _pad_cols(gz, ctx.Bp, 0.0)
         gy = torch.empty_like(gzp)
         gl = torch.empty_like(lp)
         ws.set_stream()
         L.whit_backward(gzp, ws, z, gy, gl)
         gw = None
-        if ctx.yp is not None:
-            gw = torch.empty_like(keep[0])
-            L.whit_grad_w(ws, ctx.yp, z, gy, gw)
+        if ctx.need_w:
+            gw = torch.empty_like(wp)
+            L.whit_grad_w(ws, yp, z, gy, gw)
         B = ctx.B
         if ctx.Bp != B:
             gy, gl = gy[..., :B], gl[..., :B]

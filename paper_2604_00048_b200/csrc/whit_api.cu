@@ -156,6 +156,20 @@ struct DeviceGuard {
   }
 };
 
+// Every forward records, in one place, what its backward will consume: the weights it read (float
+// plane or bit-packed), lambda, z, the dates of an irregular grid.  (A stale field -- e.g. the bit
+// plane of an earlier whit_forward_wbits -- would silently steer the next backward.)
+void mark_forward(whit_ws* ws, const void* w, const void* lam, const void* z, const uint32_t* wbits,
+                  const void* times) {
+  ws->have_fwd = true;
+  ws->have_info = true;
+  ws->w = w;
+  ws->lam = lam;
+  ws->z = z;
+  ws->wbits = wbits;
+  ws->times = times;
+}
+
 using whit_detail::kSmemBudget;
 using whit_detail::launch;
 using whit_detail::launch_irr;
@@ -456,9 +470,7 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   ws->have_fwd = false;
   st = dispatch<false>(ws, p);
   if (st != WHIT_OK) return st;
-  ws->have_fwd = true;
-  ws->have_info = true;
-  ws->w = w; ws->lam = lambda; ws->z = z; ws->wbits = nullptr;
+  mark_forward(ws, w, lambda, z, nullptr, nullptr);
   return WHIT_OK;
 }
 
@@ -485,9 +497,7 @@ whit_status whit_forward_wbits(const void* y, const uint32_t* wbits, const void*
   ws->have_fwd = false;
   st = dispatch_wb<false>(ws, p);
   if (st != WHIT_OK) return st;
-  ws->have_fwd = true;
-  ws->have_info = true;
-  ws->w = wbits; ws->lam = lambda; ws->z = z; ws->wbits = wbits;
+  mark_forward(ws, wbits, lambda, z, wbits, nullptr);
   return WHIT_OK;
 }
 
@@ -533,9 +543,7 @@ whit_status whit_forward_times_bands(const void* y, const void* w, const void* l
   ws->have_fwd = false;
   st = dispatch_irr<false>(ws, p);
   if (st != WHIT_OK) return st;
-  ws->have_fwd = true;
-  ws->have_info = true;
-  ws->w = w; ws->lam = lambda; ws->z = z; ws->times = times;
+  mark_forward(ws, w, lambda, z, nullptr, times);
   return WHIT_OK;
 }
 
@@ -577,9 +585,7 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
   else
     st = pd ? dispatch_loss_d<double, true>(d, p, ws->stream) : dispatch_loss_d<double, false>(d, p, ws->stream);
   if (st != WHIT_OK) return st;
-  ws->have_fwd = true;
-  ws->have_info = true;
-  ws->w = w; ws->lam = lambda; ws->z = z;
+  mark_forward(ws, w, lambda, z, nullptr, nullptr);
   return WHIT_OK;
 }
 

@@ -188,6 +188,23 @@ template <typename IO> struct Newton { static constexpr int N = sizeof(IO) == 4 
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000LL); }
 
+// Pivot test of row t (status, R-8): D_t must be a positive NORMAL double below 2^1022, i.e. finite,
+// > 0, and with a normal reciprocal.  Biased exponent 1..2044 with the sign bit clear; integer ALU
+// work only (no fp64-pipe compare).  A positive subnormal pivot (or one >= 2^1022) has no normal
+// reciprocal -- the MUFU seed flushes it -- so it is reported as a failure instead of producing
+// silent Inf/NaN with info = 0.  (Exact arithmetic on real data never comes near either bound.)
+__device__ __forceinline__ bool pivot_ok(double Dt) {
+  return ((static_cast<unsigned>(__double2hiint(Dt)) >> 20) - 1u) < 2044u;
+}
+
+// LAPACK-style status from the up sweep: bad = 1-based first failing pivot row (0: none);
+// nobs < d days observed means Omega is singular (for lambda > 0) with the zero pivot at row T-d,
+// so T-d+1 -- unless a pivot had already failed before that row.
+__device__ __forceinline__ int status_info(int bad, int nobs, int d, int T) {
+  if (nobs >= d) return bad;
+  return (bad != 0 && bad <= T - d) ? bad : T - d + 1;
+}
+
 template <typename IO> __device__ __forceinline__ double to_f64(IO v) { return static_cast<double>(v); }
 template <typename IO> __device__ __forceinline__ IO from_f64(double v) { return static_cast<IO>(v); }
 
@@ -442,7 +459,7 @@ struct Sweep {
       ldl_step<D, Newton<IO>::N>(st, w, lt, bb, A, Dt, idt, vt);
       if (!BWD) {
         if (!WB) nobs += (wio > IO(0));  // (WB: counted per chunk with popc)
-        pos = pos && (Dt > 0.0);  // all pivots positive (false on NaN); exact index found in a cold path
+        pos = pos && pivot_ok(Dt);  // all pivots valid (false on NaN); exact index found in a cold path
       }
     }
   }
@@ -482,7 +499,7 @@ struct Sweep {
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double A[D], Dt, idt, vt;
       ldl_step<D, Newton<IO>::N>(st, w, lt, bb, A, Dt, idt, vt);
-      if (!(Dt > 0.0)) return t + 1;
+      if (!pivot_ok(Dt)) return t + 1;
     }
     return 0;
   }
@@ -688,8 +705,9 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   // derived from it (z, D z, w*u, -(D u)(D z)) is NaN without per-store checks.
   bool failed;
   if (!BWD) {
-    if (valid) p.info[b] = (nobs < D) ? (T - D + 1) : bad;
-    failed = (nobs < D) || !allpos;
+    const int info = status_info(bad, nobs, D, T);
+    if (valid) p.info[b] = info;
+    failed = info != 0 || !allpos;
   } else {
     failed = valid ? (p.info[b] != 0) : true;
   }
@@ -973,8 +991,7 @@ __global__ void __maxnreg__((D == 3 ? 224 : 168)) whit_irr_kernel(const __grid_c
   state_init<D>(S.f);
 #pragma unroll
   for (int i = 0; i < D; ++i) binomial_col<D>(S.mu[i]);
-  int nobs = 0;
-  bool allpos = true;
+  int nobs = 0, bad = 0;  // bad: 1-based first failing pivot row
   int it = 0;
   // ================================================================ up sweep
   for (int c = 0; c < C; ++c, ++it) {
@@ -1020,7 +1037,7 @@ __global__ void __maxnreg__((D == 3 ? 224 : 168)) whit_irr_kernel(const __grid_c
         ldl_step_irr<D, NW>(S, mu_t, w, lt, bb, A, Dt, idt, vt);
         if (!BWD) {
           nobs += (wio > IO(0));
-          allpos = allpos && (Dt > 0.0);
+          if (bad == 0 && !pivot_ok(Dt)) bad = t + 1;
         }
       }
     };
@@ -1034,8 +1051,9 @@ __global__ void __maxnreg__((D == 3 ? 224 : 168)) whit_irr_kernel(const __grid_c
   }
   bool failed;
   if (!BWD) {
-    if (valid) p.info[b] = (nobs < D) ? (T - D + 1) : (allpos ? 0 : -1);
-    failed = (nobs < D) || !allpos;
+    const int info = status_info(bad, nobs, D, T);
+    if (valid) p.info[b] = info;
+    failed = info != 0;
   } else {
     failed = valid ? (p.info[b] != 0) : true;
   }
@@ -1241,8 +1259,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
 
   FState<D> st;
   state_init<D>(st);
-  int nobs = 0;
-  bool allpos = true;
+  int nobs = 0, bad = 0;  // bad: 1-based first failing pivot row
   int it = 0;
   // ---------------------------------------------------------------- up sweep: factor only
   for (int c = 0; c < C; ++c, ++it) {
@@ -1274,7 +1291,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
         double A[D], Dt, idt, vt;
         ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, A, Dt, idt, vt);
         nobs += (wio > IO(0));
-        allpos = allpos && (Dt > 0.0);
+        if (bad == 0 && !pivot_ok(Dt)) bad = t + 1;
       }
     };
     if (t0 + K > TmD) up_rows(std::true_type{});
@@ -1285,8 +1302,9 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
       issue_tile_var<D, IO, PD>(p, ring + s * V::STAGE, &bars[s], it + ST, C, (int)bw);
     }
   }
-  const bool failed = (nobs < D) || !allpos;
-  if (valid) p.info[b] = failed ? ((nobs < D) ? (T - D + 1) : -1) : 0;  // -1: pivot failure, row not located
+  const int info = status_info(bad, nobs, D, T);
+  if (valid) p.info[b] = info;
+  const bool failed = info != 0;
   const double poison = failed ? qnan() : 0.0;
 
   // ---------------------------------------------------------------- down sweep: Takahashi

@@ -147,8 +147,7 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
     state_init<D>(st);
 #pragma unroll
     for (int i = 0; i < D; ++i) binomial_col<D>(S.mu[i]);
-    int nobs = 0;
-    bool allpos = true;
+    int nobs = 0, bad = 0;  // bad: 1-based first failing pivot row
     int it = 0, fb = 0;  // fb: factor-buffer sequence number
     // one factor row: daily grid (ldl_step, binomial stencil) or uneven dates (R-18: stencil of
     // column t from the dates tile, Lambda~_t = lambda_t c_{t,0}^2, ldl_step_irr)
@@ -218,7 +217,7 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
           FW[k * 32] = wio;
           if (!BWD && (!EDGE || t < T)) {
             nobs += (wio > IO(0));
-            allpos = allpos && (Dt > 0.0);
+            if (bad == 0 && !pivot_ok(Dt)) bad = t + 1;
           }
         }
       };
@@ -233,8 +232,9 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
     }
     bool failed;
     if (!BWD) {
-      if (valid) p.info[b] = (nobs < D) ? (T - D + 1) : (allpos ? 0 : -1);
-      failed = (nobs < D) || !allpos;
+      const int info = status_info(bad, nobs, D, T);
+      if (valid) p.info[b] = info;
+      failed = info != 0;
     } else {
       failed = valid ? (p.info[b] != 0) : true;
     }

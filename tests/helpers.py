@@ -72,3 +72,26 @@ def host_inputs(x: dict, dtype=None):
         a = v.detach().cpu().to(torch.float64).numpy()
         out[k] = a.T.copy() if a.ndim == 2 else a.copy()
     return out
+
+
+def check_scalar_lambar(got, ref, abs_terms, tol, label="", well_ratio=100.0):
+    """Scalar-lambda gradient gate (R-9), two-sided.
+
+    dL/dlambda = sum_r -(Du)_r (Dz)_r is a sum whose rounding scale is sum_r |(Du)_r (Dz)_r|, so the
+    primary gate is |got - ref| / sum|terms| <= tol.  That alone is loose where the sum cancels, so
+    every series whose cancellation ratio sum|terms| / |ref| is below ``well_ratio`` must ALSO meet
+    |got - ref| / |ref| <= tol.  Returns (worst ratio, worst |ref|-relative error on the
+    well-conditioned series, number of well-conditioned series)."""
+    got = np.atleast_1d(np.asarray(got, dtype=np.float64))
+    ref = np.atleast_1d(np.asarray(ref, dtype=np.float64))
+    den = np.atleast_1d(np.asarray(abs_terms, dtype=np.float64))
+    err = np.abs(got - ref)
+    e_sum = err / np.where(den > 0, den, 1.0)
+    assert e_sum.max() <= tol, f"{label} lambar err vs sum|terms| {e_sum.max():.3e}"
+    ratio = den / np.maximum(np.abs(ref), 1e-300)
+    well = ratio < well_ratio
+    e_rel = err[well] / np.abs(ref[well]) if well.any() else np.zeros(1)
+    assert e_rel.max() <= tol, f"{label} lambar err vs |lambar| {e_rel.max():.3e} (ratio < {well_ratio})"
+    print(f"{label} scalar lambar: worst cancellation ratio {ratio.max():.3g}, |lambar|-relative error "
+          f"{e_rel.max():.3e} on {int(well.sum())}/{well.size} well-conditioned series")
+    return float(ratio.max()), float(e_rel.max()), int(well.sum())

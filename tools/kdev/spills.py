@@ -1,6 +1,8 @@
-"""Per-kernel registers / spills from paper_2604_00048_b200/build.log (ptxas -v)."""
-import re, sys
-s = open(sys.argv[1] if len(sys.argv) > 1 else "paper_2604_00048_b200/build.log").read()
+"""Per-kernel registers / spills from the ptxas -v logs (paper_2604_00048_b200/build/*.log).
+Usage: spills.py [log-glob] [all]"""
+import glob, re, sys
+pat = sys.argv[1] if len(sys.argv) > 1 else "paper_2604_00048_b200/build/*.log"
+s = "\n".join(open(f).read() for f in sorted(glob.glob(pat)))
 cur, spill = None, (0, 0)
 for line in s.splitlines():
     m = re.search(r"Compiling entry function '(\S+)'", line)
