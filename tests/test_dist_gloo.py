@@ -78,3 +78,42 @@ def test_strong_scaling_shards_cover_the_job():
 def test_max_over_ranks_without_group_is_identity():
     import bench
     assert bench.max_over_ranks(3.25) == 3.25
+
+
+def _bench(*args, timeout=600):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                            "MASTER_PORT")}
+    env["CUDA_VISIBLE_DEVICES"] = ""  # CPU host: the plumbing runs over gloo
+    return subprocess.run([sys.executable, "bench.py", *args], cwd=root, capture_output=True, text=True,
+                          timeout=timeout, env=env)
+
+
+def _json_lines(out):
+    import json
+    return [json.loads(l) for l in out.stdout.splitlines() if l.strip().startswith("{")]
+
+
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_self_launch_world2_dist_check(scaling):
+    """`python bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run with two
+    ranks -- the code path a SCALE run takes -- and the multi-process plumbing (rank-keyed shards,
+    barrier, max over ranks, checksum gather) checks out over gloo: one line, from rank 0."""
+    out = _bench("--gpus", "2", "--dist-check", "--scaling", scaling)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = _json_lines(out)
+    assert len(lines) == 1, out.stdout
+    d = lines[0]
+    assert d["dist_check"] is True and d["world_size"] == 2 and d["backend"] == "gloo"
+    assert d["scaling"] == scaling and len(d["checksums"]["per_rank"]) == 2
+
+
+def test_bench_self_launch_world2_reference_arm():
+    """--impl reference under the self-launch at N = 2: rank 0 alone times the oracle and prints one line."""
+    out = _bench("--gpus", "2", "--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-sample", "2",
+                 "--config", "toy")
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = _json_lines(out)
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["value"] > 0

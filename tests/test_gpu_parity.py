@@ -1050,7 +1050,6 @@ def test_scalar_lambda_mse_cotangent(d, dtype):
     z, gz, gy = torch.empty_like(y), torch.empty_like(y), torch.empty_like(y)
     gl, loss = torch.empty_like(lam), torch.empty(B, dtype=dtype, device="cuda")
     P.whit_forward_mse(y, w2, lam, lw, d, T, B, z, gz, loss, ws)
-    P.whit_backward(gz, ws, z, gy, gl)
     assert P.whit_failures(ws) == 0
     torch.cuda.synchronize()
     h = host_inputs({"y": y, "w": w2, "lam": lam})
@@ -1058,12 +1057,17 @@ def test_scalar_lambda_mse_cotangent(d, dtype):
     zr, _, info = O2.forward_banded(h["y"], h["w"], h["lam"], d)
     assert np.all(info == 0)
     loss_r, g_r = O1.mse_loss_grad(zr, h["y"], lwh)
-    lam_rep = np.repeat(h["lam"][:, None], T - d, 1)
-    ybar_r, terms = O2.backward_banded(g_r.astype(np.float64), h["w"], lam_rep, d, zr)
-    lambar_r = terms.sum(axis=1)
     tz, tg = TOL[(dtype, d)]
     assert rel_series(loss.double().cpu().numpy()[:, None], np.asarray(loss_r, dtype=np.float64)[:, None]).max() <= tg
     assert rel_series(gz.double().cpu().numpy().T, g_r).max() <= tg
+    # the backward of both sides takes the ORACLE's cotangent, rounded once to the I/O dtype (so an fp32
+    # rounding of g, amplified by the condition of Omega at d = 3, is not charged to the kernel)
+    g_io = torch.from_numpy(g_r.astype(np.float64).T.copy()).to(dtype)
+    P.whit_backward(g_io.cuda().contiguous(), ws, z, gy, gl)
+    torch.cuda.synchronize()
+    lam_rep = np.repeat(h["lam"][:, None], T - d, 1)
+    ybar_r, terms = O2.backward_banded(g_io.double().numpy().T, h["w"], lam_rep, d, zr)
+    lambar_r = terms.sum(axis=1)
     assert rel_series(gy.double().cpu().numpy().T, ybar_r).max() <= tg
     _, _, n_well = check_scalar_lambar(gl.double().cpu().numpy(), lambar_r.astype(np.float64),
                                        np.sum(np.abs(terms.astype(np.float64)), axis=1), tg, f"mse d={d}")
