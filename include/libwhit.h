@@ -57,8 +57,12 @@
  *   (xPBTRF "info") in the workspace: info[b] = 0 success; T-d+1 if fewer
  *   than d days have w > 0 (Omega = W + D^T Lambda D is then singular for
  *   lambda > 0: a nonzero polynomial of degree < d vanishing on every
- *   observed day has zero objective); otherwise t+1 for the first pivot
- *   D_t <= 0 or non-finite.  Read it with whit_failures().
+ *   observed day has zero objective) -- unless an earlier pivot already
+ *   failed; otherwise t+1 for the first pivot row t whose D_t is not a
+ *   positive normal double below 2^1022 (D_t <= 0, NaN, Inf, or a subnormal /
+ *   huge pivot whose reciprocal is not a normal double: DESIGN.md R-8).  This
+ *   holds for every kernel family (single series, multi-band, irregular grid,
+ *   posterior variance).  Read it with whit_failures().
  */
 #ifndef LIBWHIT_H
 #define LIBWHIT_H
@@ -136,6 +140,12 @@ void whit_ws_destroy(whit_ws* ws);
  *   factor_ws                 receives the state the backward reuses; w and
  *                             lambda must stay valid and unmodified until the
  *                             matching whit_backward has run.
+ * Binary W: the forward checks every weight; for each warp of 32
+ * series whose weights are all exactly 0 or 1 it writes W as a bit plane
+ * (1 bit per date) into factor_ws, and its own back substitution and the
+ * matching whit_backward read those bits instead of the float w rows (fewer
+ * HBM bytes; results bitwise identical).  Soft weights keep the float path.
+ * WHIT_WDET=0 in the environment turns the detection off (A/B runs).
  * One kernel launch. */
 whit_status whit_forward(const void* y, const void* w, const void* lambda, int d, int64_t T,
                          int64_t B, void* z, whit_ws* factor_ws);
@@ -179,8 +189,9 @@ whit_status whit_grad_w(whit_ws* factor_ws, const void* y, const void* z, const 
  * the band warps through shared memory (two bands per band warp), so w,
  * lambda and factor-checkpoint bytes and the factor's fp64 work are amortised
  * over C bands; every band's z and grad_y equal the single-band results bit
- * for bit.  info (one per pixel): T-d+1 (< d observed days), -1 (another
- * non-positive pivot; the single-band kernels report its exact row).  The
+ * for bit.  info (one per pixel): the status rule of "Numerical failure"
+ * (first failing pivot row of the shared factor, T-d+1 for < d observed
+ * days).  The
  * single-band entry points above are the C = 1 case (whit_forward on a C > 1
  * workspace is WHIT_ERR_SHAPE; whit_backward works for any C). */
 size_t whit_ws_bytes_bands(int d, int64_t T, int64_t B, int C, whit_dtype dtype, whit_lambda_mode lambda_mode);
@@ -269,8 +280,8 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
  * Takahashi's selected inversion on the same deviation-form banded factor
  * (one up sweep, one down sweep; only the d x d window of Omega^{-1} next to
  * the diagonal is ever formed).  w, lambda, d, T, B as in whit_forward; var
- * [T][B] output.  Uses factor_ws's checkpoint area and info[] (info = T-d+1
- * for fewer than d observed days, -1 for another non-positive pivot, var NaN);
+ * [T][B] output.  Uses factor_ws's checkpoint area and info[] (the status
+ * rule of "Numerical failure" above: first failing pivot row, var NaN);
  * if (w, lambda) differ from the last forward's, that forward's backward is
  * invalidated (WHIT_ERR_STATE).  Single-band workspaces only.  One launch. */
 whit_status whit_posterior_variance(const void* w, const void* lambda, int d, int64_t T, int64_t B, void* var,
@@ -284,6 +295,13 @@ whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info);
 /* Device pointer to the workspace's info[B] (int32), for callers that want to
  * consume it on the device without a synchronisation. */
 const int32_t* whit_info_device(const whit_ws* ws);
+
+/* SYNCHRONISES the workspace stream, then reports how many of the last plain
+ * whit_forward's warps (groups of 32 consecutive series) found a binary W and
+ * read it as bits (*n_binary) out of *n_warps = ceil(B/32).  *n_binary = 0 if
+ * the last forward was not the plain float-W forward or the detection is off.
+ * Diagnostic (tests, bench); WHIT_ERR_STATE if no forward ran. */
+whit_status whit_wbits_detected(whit_ws* ws, int64_t* n_binary, int64_t* n_warps);
 
 /* ---------------------------------------------------------------------------
  * Streaming executor for data in HOST memory.

@@ -39,6 +39,7 @@ SIGNATURES = [
     ("whit_grad_w", ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
     ("whit_failures", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int32)]),
     ("whit_info_device", _VP, [_VP]),
+    ("whit_wbits_detected", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("whit_ws_bytes_bands", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("whit_ws_create_bands", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, _VP, _SZ, _VP]),
@@ -262,6 +263,13 @@ def whit_failures(ws: Workspace, with_info: bool = False):
         return int(n.value), np.frombuffer(info, dtype=np.int32).copy()
     _check(_lib.whit_failures(ws.handle, ctypes.byref(n), None), "whit_failures")
     return int(n.value)
+
+
+def whit_wbits_detected(ws: Workspace):
+    """(warps that read W as bits, warps) of the last plain whit_forward on ws (synchronises)."""
+    nb, nw = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(_lib.whit_wbits_detected(ws.handle, ctypes.byref(nb), ctypes.byref(nw)), "whit_wbits_detected")
+    return int(nb.value), int(nw.value)
 
 
 def whit_host_ws_bytes(d: int, T: int, chunk: int, dtype, per_date: bool, nbuf: int) -> int:

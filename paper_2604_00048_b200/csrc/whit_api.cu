@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -53,7 +54,7 @@ static_assert(whit::Tile<float, 1, false>::K == whit::Tile<double, 2, true>::K &
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-  size_t off_dz, off_ckfac, off_ckrf, off_ckrb, off_info, off_cnt, total;
+  size_t off_dz, off_ckfac, off_ckrf, off_ckrb, off_info, off_cnt, off_wbits, off_wflag, total;
 };
 
 // Workspace of nb bands x B pixels: D z cache [nb][T-d][B] (I/O dtype), factor
@@ -74,6 +75,9 @@ bool layout(int d, int64_t T, int64_t B, int nb, whit_dtype dt, WsLayout* L, int
   L->off_ckrb = o;  o = align256(o + size_t(C) * nb * d * size_t(B) * 8);
   L->off_info = o;  o = align256(o + size_t(B) * 4);
   L->off_cnt = o;   o = align256(o + 8);
+  // binary-W detection of the plain forward: the bit plane of W [ceil(T/32)][B] and one flag per warp
+  L->off_wbits = o; o = align256(o + size_t((T + 31) / 32) * size_t(B) * 4);
+  L->off_wflag = o; o = align256(o + size_t((B + 31) / 32) * 4);
   L->total = o;
   return true;
 }
@@ -114,6 +118,15 @@ whit_status encode_map(CUtensorMap* m, const void* ptr, whit_dtype dt, int64_t i
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Binary-W detection in the plain forward: on unless WHIT_WDET=0 in the environment (A/B runs).
+bool wdet_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("WHIT_WDET");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
 struct whit_ws {
@@ -125,6 +138,7 @@ struct whit_ws {
   bool irr;    // irregular acquisition grid (NEXT-2): forward must be whit_forward_times
   const void* times;
   const uint32_t* wbits;  // bit-packed W of the last forward (whit_forward_wbits), else NULL
+  bool wdet;              // the last forward was the plain float-W forward with binary-W detection on
   whit_dtype dt;
   whit_lambda_mode lm;
   char* buf;
@@ -132,7 +146,8 @@ struct whit_ws {
   cudaStream_t stream;
   WsLayout L;
   bool have_fwd;   // a forward ran and its checkpoints are intact (whit_backward may follow)
-  bool have_info;  // info[] holds the status of the last forward or posterior variance
+  bool have_info;  // info[] holds the status of the last forward or posterior variance (count_failures also
+                   // counts the nonzero per-warp binary-W flags for whit_wbits_detected)
   const void* w;
   const void* lam;
   const void* z;
@@ -160,7 +175,8 @@ struct DeviceGuard {
 // plane or bit-packed), lambda, z, the dates of an irregular grid.  (A stale field -- e.g. the bit
 // plane of an earlier whit_forward_wbits -- would silently steer the next backward.)
 void mark_forward(whit_ws* ws, const void* w, const void* lam, const void* z, const uint32_t* wbits,
-                  const void* times) {
+                  const void* times, bool wdet = false) {
+  ws->wdet = wdet;
   ws->have_fwd = true;
   ws->have_info = true;
   ws->w = w;
@@ -424,7 +440,7 @@ static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, 
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
-  ws->have_fwd = false; ws->have_info = false; ws->w = ws->lam = ws->z = nullptr;
+  ws->have_fwd = false; ws->have_info = false; ws->wdet = false; ws->w = ws->lam = ws->z = nullptr;
   ws->device = -1;
   int dev = -1;
   if (cudaGetDevice(&dev) == cudaSuccess) ws->device = dev;
@@ -467,10 +483,16 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   p.out1 = ws->buf + ws->L.off_dz;
   if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
   if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
+  const bool wdet = C == 1 && wdet_enabled();
+  if (wdet) {
+    p.wbits_out = reinterpret_cast<uint32_t*>(ws->buf + ws->L.off_wbits);
+    p.wbits = p.wbits_out;
+    p.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
+  }
   ws->have_fwd = false;
   st = dispatch<false>(ws, p);
   if (st != WHIT_OK) return st;
-  mark_forward(ws, w, lambda, z, nullptr, nullptr);
+  mark_forward(ws, w, lambda, z, nullptr, nullptr, wdet);
   return WHIT_OK;
 }
 
@@ -627,6 +649,10 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
     p.wbits = ws->wbits;
     return dispatch_wb<true>(ws, p);
   }
+  if (ws->wdet) {  // the forward's binary-W bit plane and per-warp flags (the float plane is read otherwise)
+    p.wbits = reinterpret_cast<const uint32_t*>(ws->buf + ws->L.off_wbits);
+    p.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
+  }
   return dispatch<true>(ws, p);
 }
 
@@ -704,6 +730,29 @@ whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "whit_failures: %s", cudaGetErrorString(e));
   *n_failed = (int64_t)h;
+  return WHIT_OK;
+}
+
+whit_status whit_wbits_detected(whit_ws* ws, int64_t* n_binary, int64_t* n_warps) {
+  if (!ws || !n_binary || !n_warps) return fail(WHIT_ERR_ARG, "NULL argument");
+  if (!ws->have_info) return fail(WHIT_ERR_STATE, "no forward has run on this workspace");
+  const long long nw = (ws->B + 31) / 32;
+  *n_warps = nw;
+  *n_binary = 0;
+  if (!ws->wdet) return WHIT_OK;
+  DeviceGuard guard(ws->device);
+  auto* cnt = reinterpret_cast<unsigned long long*>(ws->buf + ws->L.off_cnt);
+  const int32_t* flags = reinterpret_cast<const int32_t*>(ws->buf + ws->L.off_wflag);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof *cnt, ws->stream);
+  if (e == cudaSuccess) {
+    whit::count_failures<<<(unsigned)std::min<long long>((nw + 255) / 256, 4096), 256, 0, ws->stream>>>(flags, nw, cnt);
+    e = cudaGetLastError();
+  }
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, ws->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "whit_wbits_detected: %s", cudaGetErrorString(e));
+  *n_binary = (int64_t)h;
   return WHIT_OK;
 }
 

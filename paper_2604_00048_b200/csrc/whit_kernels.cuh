@@ -65,7 +65,11 @@ struct Params {
   CUtensorMap tm_out2;    // LOSS: grad_z = dL/dz [1][T][B], box {32, K, 1} (TMA store)
   void* loss;             // LOSS: per-series loss [B]
   void* out2;             // LOSS: grad_z = dL/dz [T][B] (direct coalesced stores)
-  const uint32_t* wbits;  // WB: bit-packed 0/1 weights [ceil(T/32)][B], bit t%32 of word t/32
+  const uint32_t* wbits;  // WB: bit-packed 0/1 weights [ceil(T/32)][B], bit t%32 of word t/32 (caller's, or
+                          // the plane the plain forward wrote: binary-W detection, WD below)
+  uint32_t* wbits_out;    // WD forward: the bit plane of W [ceil(T/32)][B] it writes (workspace)
+  int32_t* wflag;         // WD: per-warp flag [ceil(B/32)]: 1 if all 32 series' w are exactly 0 / 1
+                          // (forward writes it, backward reads it; NULL: detection off)
   double* ck_fac;         // factor checkpoints [C][NFAC][B] (forward up sweep; read by every later sweep)
   double* ck_rhs_f;       // forward rhs checkpoints [C][nb][d][B]
   double* ck_rhs_b;       // backward rhs checkpoints [C][nb][d][B]
@@ -184,7 +188,10 @@ __device__ __forceinline__ double rcp64(double x) {
   }
   return r;
 }
-template <typename IO> struct Newton { static constexpr int N = sizeof(IO) == 4 ? 1 : 2; };
+// fp32 I/O at d <= 2: one step (~2^-44, four orders below what fp32 outputs can show).  d = 3 takes two
+// steps in fp32 I/O too: its Omega is ill-conditioned enough (long gaps) that a 1e-13 pivot error
+// reaches the 3rd differences D z (and so dL/dlambda) at the 1e-2 level on small-|D z| series.
+template <typename IO, int D> struct Newton { static constexpr int N = (sizeof(IO) == 4 && D <= 2) ? 1 : 2; };
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000LL); }
 
@@ -385,16 +392,18 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
 };
 
 // Issue tile i (up sweep tiles 0..C-1, then down sweep C-1..0) of one warp.
+// skip_w (binary W detected, WD): the tile's w rows are not loaded -- the consumer reads the bit plane.
 template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
 __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage, uint64_t* bar, int i, int C,
-                                           int c0, int band) {
+                                           int c0, int band, bool skip_w = false) {
   using L = Layout<D, IO, PD, BWD, LOSS, WB>;
   const bool up = i < C;
   const int c = up ? i : 2 * C - 1 - i;
   const int t0 = c * L::K;
-  mbar_arrive_expect_tx(bar, up ? L::BYTES_UP : L::BYTES_DN);
+  const bool load_w = !WB && !skip_w;
+  mbar_arrive_expect_tx(bar, (up ? L::BYTES_UP : L::BYTES_DN) - (load_w || WB ? 0u : uint32_t(L::K * L::ROW)));
   tma_load_3d(stage + L::OFF_RHS, &p.tm_rhs, c0, t0, band, bar);
-  if (!WB) tma_load_2d(stage + L::OFF_W, &p.tm_w, c0, t0, bar);
+  if (load_w) tma_load_2d(stage + L::OFF_W, &p.tm_w, c0, t0, bar);
   if (PD) {
     if (up) tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_up, c0, t0, bar);
     else tma_load_2d(stage + L::OFF_LAM, &p.tm_lam_dn, c0, t0 - D, bar);
@@ -419,10 +428,12 @@ __device__ __forceinline__ void issue_tile(const Params& p, unsigned char* stage
 }
 
 // ------------------------------------------------------------------ per-thread sweep bodies
-// Weight of row k of a chunk: from the staged w tile, or (WB) bit k of the chunk's mask.
-template <typename IO, bool WB>
-__device__ __forceinline__ void row_w(const IO* t_w, uint32_t wm, int k, IO& wio, double& w) {
-  if (WB) {
+// Weight of row k of a chunk: from the staged w tile, or (ub: bit-packed W -- the caller's (WB) or the
+// plane the forward wrote after detecting a binary W) bit k of the chunk's mask.  A bit reconstructs
+// w_t = 1 / 0 exactly, so every downstream value is bitwise the float-plane one.
+template <typename IO>
+__device__ __forceinline__ void row_w(const IO* t_w, uint32_t wm, int k, IO& wio, double& w, bool ub) {
+  if (ub) {
     const bool on = (wm >> k) & 1u;
     wio = on ? IO(1) : IO(0);
     w = on ? 1.0 : 0.0;
@@ -432,15 +443,29 @@ __device__ __forceinline__ void row_w(const IO* t_w, uint32_t wm, int k, IO& wio
   }
 }
 
+// Binary-W detection (WD): is this weight exactly +0 or 1 (bit patterns; -0, soft weights, NaN: no)?
+template <typename IO> __device__ __forceinline__ bool w_is_binary(IO v);
+template <> __device__ __forceinline__ bool w_is_binary<float>(float v) {
+  const unsigned u = __float_as_uint(v);
+  return (u == 0u) | (u == 0x3f800000u);
+}
+template <> __device__ __forceinline__ bool w_is_binary<double>(double v) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (u == 0ull) | (u == 0x3ff0000000000000ull);
+}
+
 template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
 struct Sweep {
   using L = Layout<D, IO, PD, BWD, LOSS, WB>;
   static constexpr int K = L::K;
 
   // ---- up sweep over one chunk (rows t0..t0+K-1); RAGGED: the chunk reaches row T-D or beyond
+  // WD (plain forward): also gathers the chunk's mask bits (cb) and whether every w is exactly 0 / 1.
+  static constexpr bool WD = !BWD && !LOSS && !WB;
   template <bool RAGGED>
   static __device__ __forceinline__ void up_chunk(FState<D>& st, const unsigned char* stg, int lane, int t0, int T,
-                                                  double lam_s, int& nobs, bool& pos, uint32_t wm = 0) {
+                                                  double lam_s, int& nobs, bool& pos, uint32_t wm, bool ub,
+                                                  uint32_t& cb, bool& isbin) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;
@@ -451,12 +476,16 @@ struct Sweep {
       if (RAGGED && t >= T) break;  // rows past the end: nothing uses the state after row T-1
       IO wio;
       double w;
-      row_w<IO, WB>(t_w, wm, k, wio, w);
+      row_w<IO>(t_w, wm, k, wio, w, ub);
+      if (WD) {
+        cb |= uint32_t(wio != IO(0)) << k;
+        isbin = isbin && w_is_binary<IO>(wio);
+      }
       double lt = PD ? to_f64<IO>(t_lam[k * 32]) : lam_s;
       if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double A[D], Dt, idt, vt;
-      ldl_step<D, Newton<IO>::N>(st, w, lt, bb, A, Dt, idt, vt);
+      ldl_step<D, Newton<IO, D>::N>(st, w, lt, bb, A, Dt, idt, vt);
       if (!BWD) {
         if (!WB) nobs += (wio > IO(0));  // (WB: counted per chunk with popc)
         pos = pos && pivot_ok(Dt);  // all pivots valid (false on NaN); exact index found in a cold path
@@ -485,7 +514,7 @@ struct Sweep {
       const bool in = tj >= 0 && tj < T - D;
       const double l = !in ? 0.0 : PD ? to_f64<IO>(lam_plane[(long long)tj * B + b]) : lam_s;
       st.lm[i] = l;
-      st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO>::N>(l + st.dl[i]);
+      st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO, D>::N>(l + st.dl[i]);
     }
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
@@ -494,11 +523,11 @@ struct Sweep {
       const int t = t0 + k;
       IO wio;
       double w;
-      row_w<IO, WB>(t_w, wm, k, wio, w);
+      row_w<IO>(t_w, wm, k, wio, w, WB);
       const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : (t < T - D ? lam_s : 0.0);
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double A[D], Dt, idt, vt;
-      ldl_step<D, Newton<IO>::N>(st, w, lt, bb, A, Dt, idt, vt);
+      ldl_step<D, Newton<IO, D>::N>(st, w, lt, bb, A, Dt, idt, vt);
       if (!pivot_ok(Dt)) return t + 1;
     }
     return 0;
@@ -514,7 +543,8 @@ struct Sweep {
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
                                                     double two_over_T = 0.0, uint32_t wm = 0, IO* gz0 = nullptr,
-                                                    long long Bst = 0, bool valid = false, IO* gl0 = nullptr) {
+                                                    long long Bst = 0, bool valid = false, IO* gl0 = nullptr,
+                                                    bool ub = WB) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -527,12 +557,12 @@ struct Sweep {
       const int t = t0 + k;
       IO wio;
       double w;
-      row_w<IO, WB>(t_w, wm, k, wio, w);
+      row_w<IO>(t_w, wm, k, wio, w, ub);
       double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
       if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
       const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
       double Dt, idt, vt;
-      ldl_step<D, Newton<IO>::N>(st, w, lt, bb, Ak[k], Dt, idt, vt);
+      ldl_step<D, Newton<IO, D>::N>(st, w, lt, bb, Ak[k], Dt, idt, vt);
       q[k] = vt * idt;
       if (RAGGED && t >= T) {  // rows past the end: z = 0 exactly (q = 0, A = 0, zero window)
         q[k] = 0.0;
@@ -575,13 +605,15 @@ struct Sweep {
         }
       } else {
         IO gy, gl = IO(0);
+        IO wk;
+        double wkd;
+        row_w<IO>(t_w, wm, k, wk, wkd, ub);  // (bits: the exact 1 / 0 the float plane holds)
         if (sizeof(IO) == 4 && PD) {
           // fp32 I/O: w*u and -(Du)(Dz) formed from u, Du rounded once to fp32 (<= 1.5 ulp fp32)
-          gy = WB ? (((wm >> k) & 1u) ? from_f64<IO>(z) : IO(0)) : t_w[k * 32] * from_f64<IO>(z);
+          gy = wk * from_f64<IO>(z);
           gl = -(from_f64<IO>(dz) * t_dz[k * 32]);  // D z tile is 0 past row T-d-1
         } else {
-          const double w = WB ? (((wm >> k) & 1u) ? 1.0 : 0.0) : to_f64<IO>(t_w[k * 32]);
-          gy = from_f64<IO>(w * z);
+          gy = from_f64<IO>(wkd * z);
           const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
           if (PD) gl = from_f64<IO>(g);
           else if (!RAGGED || t < TmD) lam_acc += g;
@@ -632,12 +664,21 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   uint64_t* bars = full_bar[warp];
   const int ntiles = 2 * C;
 
+  // Binary-W detection (WD): the plain forward gathers the mask bits of its series in the up
+  // sweep, writes them to the workspace's bit plane and, if all 32 series of the warp have w in {0, 1},
+  // a per-warp flag; from then on its down sweep and both sweeps of the backward read the bits instead of
+  // the float w rows (their TMA loads are skipped).  ub: this warp reads W as bits now.
+  constexpr bool WD = S::WD;
+  constexpr bool WDB = BWD && !WB && !LOSS;
+  bool ub = WB;
+  if (WDB && p.wflag != nullptr) ub = p.wflag[bw >> 5] != 0;
+
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < ST; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < ST && i < ntiles; ++i)
-      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + i * L::STAGE, &bars[i], i, C, (int)bw, band, ub);
   }
   __syncwarp();
 
@@ -651,9 +692,10 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   int nobs = 0, bad = 0;
   bool allpos = true;
   int it = 0;
-  // WB: the chunk's mask bits, prefetched one chunk ahead (plain coalesced 4-B loads)
+  // bits of W (WB, or WD once detected): the chunk's mask bits, prefetched one chunk ahead (plain coalesced
+  // 4-B loads)
   auto wword = [&](int cc) -> uint32_t {
-    if (!WB || !valid || cc < 0 || cc >= C) return 0u;
+    if (!ub || !valid || cc < 0 || cc >= C) return 0u;
     // bits cc*K .. cc*K+K-1 of the series' mask; a chunk may straddle two words when K does not divide 32
     const int bit0 = cc * K, r = bit0 >> 5, sh = bit0 & 31;
     uint64_t two = p.wbits[(long long)r * B + b];
@@ -661,6 +703,9 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
     return (uint32_t)(two >> sh) & (K >= 32 ? 0xffffffffu : ((1u << K) - 1u));
   };
   uint32_t wm_next = wword(0);
+  uint64_t wacc = 0;   // WD: mask bits of rows wbase*32.. not yet stored
+  int wbase = 0;
+  bool isbin = true;   // WD: every w of this series so far is exactly 0 or 1
 
   // ================================================================ up sweep
   for (int c = 0; c < C; ++c, ++it) {
@@ -686,17 +731,32 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
       for (int i = 0; i < D; ++i) ck[(long long)i * B] = st.v[i];
     }
     bool pos = true;
-    if (c < cr) S::template up_chunk<false>(st, stg, lane, t0, T, lam_s, nobs, pos, wm);
-    else S::template up_chunk<true>(st, stg, lane, t0, T, lam_s, nobs, pos, wm);
+    uint32_t cb = 0;
+    if (c < cr) S::template up_chunk<false>(st, stg, lane, t0, T, lam_s, nobs, pos, wm, ub, cb, isbin);
+    else S::template up_chunk<true>(st, stg, lane, t0, T, lam_s, nobs, pos, wm, ub, cb, isbin);
     if (WB && !BWD) nobs += __popc(wm);  // bits past T are 0 (packing)
+    if (WD && p.wflag != nullptr) {  // append the chunk's K bits; store each completed 32-row word
+      wacc |= uint64_t(cb) << (t0 - wbase * 32);
+      if (t0 + K >= (wbase + 1) * 32) {
+        if (valid) p.wbits_out[(long long)wbase * B + b] = uint32_t(wacc);
+        wacc >>= 32;
+        ++wbase;
+      }
+    }
     allpos = allpos && pos;
     // exact failing row (cold path): replayed from the factor checkpoint this warp wrote
     if (!BWD && !pos && bad == 0 && valid) bad = S::first_bad_row(p, c, b, stg, lane, t0, T, lam_s, wm);
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band, ub);
     }
+  }
+  if (WD && p.wflag != nullptr) {  // last partial word, the warp's vote, and bits from here on
+    if (valid && wbase * 32 < T) p.wbits_out[(long long)wbase * B + b] = uint32_t(wacc);
+    const bool all_bin = __all_sync(0xffffffffu, isbin || !valid);
+    if (lane == 0) p.wflag[bw >> 5] = all_bin ? 1 : 0;
+    ub = all_bin;  // (this lane's own stores above are what wword() reads back)
   }
 
   // Status (LAPACK xPBTRF style): fewer than d observed days -> T-d+1 (exactly
@@ -762,7 +822,7 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
         st.v[i] = pv[i] + poison;
         const double l = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : ((tj >= 0 && tj < T - D) ? lam_s : 0.0);
         st.lm[i] = l;
-        st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO>::N>(l + pdl[i]);
+        st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO, D>::N>(l + pdl[i]);
       }
     }
     if (c > 0) WHIT_LOAD_CK(c - 1);
@@ -779,10 +839,10 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
                                                        : nullptr;
     if (c < cr)
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    nullptr, two_over_T, wm, gz0, B, valid, gl0);
+                                    nullptr, two_over_T, wm, gz0, B, valid, gl0, ub);
     else
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   nullptr, two_over_T, wm, gz0, B, valid, gl0);
+                                   nullptr, two_over_T, wm, gz0, B, valid, gl0, ub);
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
     if (lane == 0 && !L::DIRECT) {
@@ -794,7 +854,7 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
     __syncwarp();
     if (lane == 0 && it + ST < ntiles) {
       fence_proxy_async_smem();
-      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band);
+      issue_tile<D, IO, PD, BWD, LOSS, WB>(p, ring + s * L::STAGE, &bars[s], it + ST, C, (int)bw, band, ub);
     }
   }
 #undef WHIT_LOAD_CK
@@ -962,7 +1022,7 @@ __global__ void __maxnreg__((D == 3 ? 224 : 168)) whit_irr_kernel(const __grid_c
   constexpr int K = L::K, ST = L::ST, WARPS = L::WARPS;
   constexpr int UP_UNROLL = WHIT_IRR_UP_UNROLL;
   constexpr int NFAC = Ck<D>::NFAC;
-  constexpr int NW = Newton<IO>::N;
+  constexpr int NW = Newton<IO, D>::N;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t full_bar[WARPS][ST];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1289,7 +1349,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
         const double w = to_f64<IO>(wio);
         const double lt = PD ? to_f64<IO>(t_lam[k * 32]) : ((!EDGE || t < TmD) ? lam_s : 0.0);
         double A[D], Dt, idt, vt;
-        ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, A, Dt, idt, vt);
+        ldl_step<D, Newton<IO, D>::N>(st, w, lt, 0.0, A, Dt, idt, vt);
         nobs += (wio > IO(0));
         if (bad == 0 && !pivot_ok(Dt)) bad = t + 1;
       }
@@ -1345,7 +1405,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
       st.v[i] = 0.0;
       const double l = PD ? to_f64<IO>(t_lam[(D - 1 - i) * 32]) : ((tj >= 0 && tj < TmD) ? lam_s : 0.0);
       st.lm[i] = l;
-      st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO>::N>(l + st.dl[i]);
+      st.id[i] = (tj < 0) ? 1.0 : rcp64<Newton<IO, D>::N>(l + st.dl[i]);
     }
     double idk[K];
     double Ak[K][D];
@@ -1356,7 +1416,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
       double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
       if (!PD) lt = (!edge || t < TmD) ? lt : 0.0;
       double Dt, vt;
-      ldl_step<D, Newton<IO>::N>(st, w, lt, 0.0, Ak[k], Dt, idk[k], vt);
+      ldl_step<D, Newton<IO, D>::N>(st, w, lt, 0.0, Ak[k], Dt, idk[k], vt);
       if (ragged && t >= T) {  // rows past the end: Sigma = 0 there, no coupling
         idk[k] = 0.0;
 #pragma unroll

@@ -89,7 +89,7 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
 #define WHIT_MB2_IRR_BUNROLL 8
 #endif
   constexpr int BROW_UNROLL = IRR ? WHIT_MB2_IRR_BUNROLL : 8;  // band warps' up-sweep rows
-  constexpr int K = L::K, ST = L::ST, FST = L::FST, NFAC = Ck<D>::NFAC, NW = Newton<IO>::N, BPW = L::BPW;
+  constexpr int K = L::K, ST = L::ST, FST = L::FST, NFAC = Ck<D>::NFAC, NW = Newton<IO, D>::N, BPW = L::BPW;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t f_full[FST];
   __shared__ __align__(8) uint64_t b_full[(kMaxBands + 1) / 2][ST];
