@@ -129,7 +129,21 @@ bool wdet_enabled() {
 
 }  // namespace
 
+// Encoded TMA descriptors of a workspace, keyed by (pointer, dtype, shape, box): a training loop calls
+// forward / backward with the same buffers every step, so cuTensorMapEncodeTiled runs once per buffer.
+struct MapCache {
+  static constexpr int N = 24;
+  struct Key {
+    const void* ptr;
+    int64_t inner, rows;
+    int box, depth, dt;
+  } key[N];
+  CUtensorMap map[N];
+  int n = 0, next = 0;
+};
+
 struct whit_ws {
+  mutable MapCache maps;
   int device;  // CUDA device current at creation (-1: none), made current around encodes/launches
   int d;
   int64_t T, B;
@@ -154,6 +168,26 @@ struct whit_ws {
 };
 
 namespace {
+
+whit_status wmap(const whit_ws* ws, CUtensorMap* m, const void* ptr, whit_dtype dt, int64_t inner, int64_t rows,
+                 int box_rows, int depth = 0) {
+  MapCache& c = ws->maps;
+  const MapCache::Key k{ptr, inner, rows, box_rows, depth, int(dt)};
+  for (int i = 0; i < c.n; ++i) {
+    const MapCache::Key& e = c.key[i];
+    if (e.ptr == k.ptr && e.inner == k.inner && e.rows == k.rows && e.box == k.box && e.depth == k.depth &&
+        e.dt == k.dt) {
+      *m = c.map[i];
+      return WHIT_OK;
+    }
+  }
+  const whit_status st = encode_map(m, ptr, dt, inner, rows, box_rows, depth);
+  if (st != WHIT_OK) return st;
+  const int slot = c.n < MapCache::N ? c.n++ : (c.next++ % MapCache::N);
+  c.key[slot] = k;
+  c.map[slot] = *m;
+  return WHIT_OK;
+}
 
 // Makes the workspace's device current on the calling thread (autograd runs
 // backward on its own device thread, where no context is bound yet) and
@@ -299,11 +333,11 @@ whit_status fill_params(const whit_ws* ws, Params* p, const void* rhs, const voi
   const int d = ws->d;
   const int kK = ws->kk;
   whit_status st;
-  if ((st = encode_map(&p->tm_rhs, rhs, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
-  if ((st = encode_map(&p->tm_w, w, ws->dt, ws->B, ws->T, kK)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p->tm_rhs, rhs, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p->tm_w, w, ws->dt, ws->B, ws->T, kK)) != WHIT_OK) return st;
   if (ws->lm == WHIT_LAMBDA_PER_DATE) {
-    if ((st = encode_map(&p->tm_lam_up, lam, ws->dt, ws->B, ws->T - d, kK)) != WHIT_OK) return st;
-    if ((st = encode_map(&p->tm_lam_dn, lam, ws->dt, ws->B, ws->T - d, kK + d)) != WHIT_OK) return st;
+    if ((st = wmap(ws, &p->tm_lam_up, lam, ws->dt, ws->B, ws->T - d, kK)) != WHIT_OK) return st;
+    if ((st = wmap(ws, &p->tm_lam_dn, lam, ws->dt, ws->B, ws->T - d, kK + d)) != WHIT_OK) return st;
     p->lam_plane = lam;
   } else {
     p->lam_scalar = lam;
@@ -481,8 +515,8 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   const int kK = ws->kk;
   p.out0 = z;
   p.out1 = ws->buf + ws->L.off_dz;
-  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
   const bool wdet = C == 1 && wdet_enabled();
   if (wdet) {
     p.wbits_out = reinterpret_cast<uint32_t*>(ws->buf + ws->L.off_wbits);
@@ -514,8 +548,8 @@ whit_status whit_forward_wbits(const void* y, const uint32_t* wbits, const void*
   if (st != WHIT_OK) return st;
   p.wbits = wbits;
   const int kK = ws->kk;
-  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
   ws->have_fwd = false;
   st = dispatch_wb<false>(ws, p);
   if (st != WHIT_OK) return st;
@@ -559,9 +593,9 @@ whit_status whit_forward_times_bands(const void* y, const void* w, const void* l
   const int kK = ws->kk;
   p.out0 = z;  // multi-band kernel: direct stores
   p.out1 = ws->buf + ws->L.off_dz;
-  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_lw, times, ws->dt, B, T, kK + 2 * d)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_lw, times, ws->dt, B, T, kK + 2 * d)) != WHIT_OK) return st;
   ws->have_fwd = false;
   st = dispatch_irr<false>(ws, p);
   if (st != WHIT_OK) return st;
@@ -594,10 +628,10 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
   whit_status st = fill_params(ws, &p, y, w, lambda);
   if (st != WHIT_OK) return st;
   const int kK = ws->kk;
-  if ((st = encode_map(&p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_lw, loss_w, ws->dt, B, T, kK)) != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out2, grad_z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out0, z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, 1)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_lw, loss_w, ws->dt, B, T, kK)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out2, grad_z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
   p.loss = loss;
   p.out2 = grad_z;
   ws->have_fwd = false;
@@ -632,17 +666,17 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
   whit_status st = fill_params(ws, &p, grad_z, ws->w, ws->lam);
   if (st != WHIT_OK) return st;
   const int kK = ws->kk;
-  if ((st = encode_map(&p.tm_dz, ws->buf + ws->L.off_dz, ws->dt, ws->B, ws->T - ws->d, kK, ws->nb)) != WHIT_OK)
+  if ((st = wmap(ws, &p.tm_dz, ws->buf + ws->L.off_dz, ws->dt, ws->B, ws->T - ws->d, kK, ws->nb)) != WHIT_OK)
     return st;
-  if ((st = encode_map(&p.tm_out0, grad_y, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out0, grad_y, ws->dt, ws->B, ws->T, kK, ws->nb)) != WHIT_OK) return st;
   if (ws->lm == WHIT_LAMBDA_PER_DATE) {
-    if ((st = encode_map(&p.tm_out1, grad_lambda, ws->dt, ws->B, ws->T - ws->d, kK)) != WHIT_OK) return st;
+    if ((st = wmap(ws, &p.tm_out1, grad_lambda, ws->dt, ws->B, ws->T - ws->d, kK)) != WHIT_OK) return st;
   }
   p.out0 = grad_y;
   p.out1 = grad_lambda;
   p.dz_cache = ws->buf + ws->L.off_dz;
   if (ws->irr) {
-    if ((st = encode_map(&p.tm_lw, ws->times, ws->dt, ws->B, ws->T, kK + 2 * ws->d)) != WHIT_OK) return st;
+    if ((st = wmap(ws, &p.tm_lw, ws->times, ws->dt, ws->B, ws->T, kK + 2 * ws->d)) != WHIT_OK) return st;
     return dispatch_irr<true>(ws, p);
   }
   if (ws->wbits) {
@@ -701,7 +735,7 @@ whit_status whit_posterior_variance(const void* w, const void* lambda, int d, in
   Params p;
   whit_status st = fill_params(ws, &p, w /* unused rhs slot */, w, lambda);
   if (st != WHIT_OK) return st;
-  if ((st = encode_map(&p.tm_out0, var, ws->dt, B, T, ws->kk, 1)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p.tm_out0, var, ws->dt, B, T, ws->kk, 1)) != WHIT_OK) return st;
   // the factor checkpoints are shared with the forward: a different (w, lambda) invalidates its backward
   if (w != ws->w || lambda != ws->lam) ws->have_fwd = false;
   ws->have_info = true;  // (set at enqueue: info is written by this launch)

@@ -113,12 +113,15 @@ def make_inputs(cfg: Config | str, *, B: int | None = None, T: int | None = None
                 d: int | None = None, seed: int | None = None, series_offset: int = 0,
                 device="cpu", dtype=torch.float32, with_g: bool = True,
                 lam_mode: str | None = None, mask: str | None = None,
-                lam_max: float = 1e5, row_chunk_elems: int = 1 << 24, series_ids=None) -> dict:
+                lam_max: float = 1e5, row_chunk_elems: int = 1 << 24, series_ids=None,
+                last_acq: int | None = None) -> dict:
     """Draw one shard ``[series_offset, series_offset + B)`` of a config (or the
     explicit global ``series_ids``, e.g. a sample spread over the batch).
 
     Returns ``{"y": (T,B), "w": (T,B), "lam": (T-d,B) or (B,), "g": (T,B)}`` on
     ``device`` in ``dtype`` (float32 or float64), plus the config echo.
+    ``last_acq``: first date without acquisitions for the "s2" mask (default 3197, 2024-10-02, which
+    gives T = 3288 its 90-day trailing gap; the sweep passes T - 91 to keep that gap at any T).
     """
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
@@ -176,7 +179,7 @@ def make_inputs(cfg: Config | str, *, B: int | None = None, T: int | None = None
             acq = (torch.remainder(t - phase - 1, 10) == 0) & (t >= 1)
             acq |= (torch.remainder(t - phase - 6, 10) == 0) & (t >= T_S2B)
             acq |= has2 & (torch.remainder(t - phase2 - 3, 10) == 0) & (t >= 1)
-            acq &= t < T_LAST_ACQ
+            acq &= t < (T_LAST_ACQ if last_acq is None else last_acq)
             pc = 0.45 + 0.30 * torch.cos(2 * math.pi * (doy - 15.0) / 365.0)
             clear = acq & (S.per_cell(20, t) > pc)
         else:

@@ -93,5 +93,9 @@ def test_workspace_state_across_forward_variants():
     P.whit_forward(y, w, lam, d, T, B, z1, ws)                  # leaves detection flags in ws
     a = mse_bwd(ws)
     b = mse_bwd(P.Workspace(d, T, B, torch.float32, True))
-    for u, v in zip(a, b):
-        assert torch.equal(u, v)
+    for name, u, v in zip(("z", "grad_y", "grad_lambda", "grad_w"), a, b):
+        if not torch.allclose(u, v, rtol=0.0, atol=0.0, equal_nan=True):  # (held-out dates can leave a
+            bad = (u != v) & ~(torch.isnan(u) & torch.isnan(v))                 # series < d observations: NaN)
+            idx = bad.nonzero()[:8].tolist()
+            raise AssertionError(f"{name}: {int(bad.sum())} differ, first {idx}, "
+                                 f"{[(u[tuple(i)].item(), v[tuple(i)].item()) for i in idx]}")
