@@ -634,7 +634,6 @@ def run_fwdbwd(args, P, synth, dev, stream, ws_n, rank):
     ms_step, per, clocks = timed_steps(launches, args.steps, args.warmup, dev, stream)
     nfail = P.whit_failures(wsp)
     value = B_job / (ms_step / 1e3)
-    binary_w = bool(getattr(wsp, "binary_w", lambda: None)()) if hasattr(wsp, "binary_w") else None
 
     # per-rank checksums of the outputs (exact: int64 sums of the bit patterns, order-independent), gathered
     # outside the timed region.  Under weak scaling rank r owns global series [r*B, (r+1)*B) at every N, so
@@ -642,7 +641,8 @@ def run_fwdbwd(args, P, synth, dev, stream, ws_n, rank):
     checksums = gather_checksums((z,) if fwd_only else (z, gy, gl), ws_n)
     checksums["tensors"] = "z" if fwd_only else "z, grad_y, grad_lambda"
 
-    wdet = bool(P.binary_w_detect_enabled()) if hasattr(P, "binary_w_detect_enabled") else False
+    nbin, nwarps = P.whit_wbits_detected(wsp)  # warps of the last forward that read W as bits
+    wdet = nbin == nwarps and nwarps > 0
     fb, bb, mf, mb = algorithmic_bytes(B, T, d, esz, per_date, wdet=wdet)
     kb = {"whit_forward": fb} if fwd_only else {"whit_forward": fb, "whit_backward": bb}
     mins = {"whit_forward": mf} if fwd_only else {"whit_forward": mf, "whit_backward": mb}
@@ -692,8 +692,8 @@ def run_fwdbwd(args, P, synth, dev, stream, ws_n, rank):
         line = base_line(args, METRICS[args.config], value, UNIT, ws_n, ms_step, len(launches) * args.steps, config,
                          roofline=roof, clocks=clocks, e2e=e2e, cpu_baseline=cpu, cpu_banded=cpu_banded,
                          w_bits=wbits_line, e2e_wbits=e2e_wbits, checksums=checksums)
-        if binary_w is not None:
-            line["binary_w_detected"] = binary_w
+        line["binary_w"] = {"warps_reading_bits": nbin, "warps": nwarps,
+                            "how": "whit_forward detected W in {0, 1} per warp of 32 series (DESIGN §5)"}
         print(json.dumps(line), flush=True)
     return 0
 

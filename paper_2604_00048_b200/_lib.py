@@ -132,7 +132,7 @@ class Workspace:
     or an irregular-grid workspace with ``times=True``)."""
 
     def __init__(self, d: int, T: int, B: int, dtype: torch.dtype, per_date: bool, device=None, stream=None,
-                 C: int = 1, times: bool = False):
+                 C: int = 1, times: bool = False, buf: torch.Tensor | None = None):
         if times:
             nbytes = int(_lib.whit_ws_bytes_times_bands(d, T, B, C, _dtype_code(dtype), int(per_date)))
         else:
@@ -140,7 +140,13 @@ class Workspace:
         if nbytes == 0:
             raise WhitError(1, f"workspace bytes(d={d}, T={T}, B={B}, C={C}, times={times})")
         self.d, self.T, self.B, self.C, self.dtype, self.per_date = d, T, B, C, dtype, per_date
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+        if buf is not None:  # caller-provided device buffer (uint8, >= nbytes, 256-B aligned)
+            if buf.dtype != torch.uint8 or not buf.is_cuda or buf.numel() < nbytes:
+                raise ValueError(f"workspace buffer must be a CUDA uint8 tensor of >= {nbytes} bytes")
+            self.buf = buf
+        else:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+        self.nbytes = nbytes
         h = ctypes.c_void_p()
         if times:
             _check(_lib.whit_ws_create_times_bands(ctypes.byref(h), d, T, B, C, _dtype_code(dtype), int(per_date),

@@ -342,8 +342,8 @@ template <int D> struct Ck {
 #ifndef WHIT_L2_PREFETCH
 #define WHIT_L2_PREFETCH 0
 #endif
-#ifndef WHIT_BWD_DIRECT
-#define WHIT_BWD_DIRECT 1
+#ifndef WHIT_BWD_DIRECT  // backward outputs by direct stores: measured slower once W is read as bits (binary-W
+#define WHIT_BWD_DIRECT 0  // detection: 5.87 vs 5.41 ms hetero) and equal on soft W (5.58 vs 5.64): TMA stores
 #endif
 #ifndef WHIT_FWD_DIRECT  // plain forward by direct stores: measured neutral (hetero fwd 5.52-5.56 ms vs 5.51-5.55
 #define WHIT_FWD_DIRECT 0  // staged; the forward is register-limited to 12 warps/SM either way), so TMA stores stay
