@@ -296,6 +296,22 @@ whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info);
  * consume it on the device without a synchronisation. */
 const int32_t* whit_info_device(const whit_ws* ws);
 
+/* Execution path of whit_forward / whit_backward on a single-band daily-grid
+ * workspace.  Small batches take the TWISTED path (two warps per group of 32
+ * series: one factors the first half of the dates forward, the other the
+ * second half in reversed time; they meet in a d x d block -- half the
+ * per-series latency, twice the warps in flight); a group whose halves are
+ * not safely SPD on their own falls back to the sequential kernel inside the
+ * same call (results and status as the sequential path).  mode: -1 auto (the
+ * default: WHIT_TWIST=0/1 in the environment, else batches of at most two
+ * waves, B <= 113,664), 0 never, 1 whenever T allows (T >= about 4K + 2d). */
+whit_status whit_ws_set_twist(whit_ws* ws, int mode);
+
+/* SYNCHRONISES the workspace stream, then reports how many groups of 32
+ * series the last whit_forward solved on the twisted path (*n_twisted) out of
+ * *n_groups = ceil(B/32) (0 if the path was not taken).  Diagnostic. */
+whit_status whit_twist_groups(whit_ws* ws, int64_t* n_twisted, int64_t* n_groups);
+
 /* SYNCHRONISES the workspace stream, then reports how many of the last plain
  * whit_forward's warps (groups of 32 consecutive series) found a binary W and
  * read it as bits (*n_binary) out of *n_warps = ceil(B/32).  *n_binary = 0 if

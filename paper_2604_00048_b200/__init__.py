@@ -32,9 +32,10 @@ from ._lib import (  # noqa: F401
     whit_run_host_bands,
     whit_ws_bytes,
     whit_wbits_detected,
+    whit_twist_groups,
 )
 from .autograd import WhittakerFn, smooth  # noqa: F401
 
 __all__ = ["smooth", "WhittakerFn", "Workspace", "whit_forward", "whit_backward", "whit_failures",
            "whit_ws_bytes", "whit_forward_bands", "whit_backward_bands", "whit_grad_w",
-           "whit_ws_bytes_bands", "whit_forward_mse", "whit_forward_times", "whit_forward_times_bands", "whit_forward_wbits", "whit_pack_mask", "whit_posterior_variance", "whit_host_ws_bytes", "whit_run_host", "whit_run_host_bands", "whit_wbits_detected", "WhitError", "WHIT_F32", "WHIT_F64"]
+           "whit_ws_bytes_bands", "whit_forward_mse", "whit_forward_times", "whit_forward_times_bands", "whit_forward_wbits", "whit_pack_mask", "whit_posterior_variance", "whit_host_ws_bytes", "whit_run_host", "whit_run_host_bands", "whit_wbits_detected", "whit_twist_groups", "WhitError", "WHIT_F32", "WHIT_F64"]

@@ -40,6 +40,8 @@ SIGNATURES = [
     ("whit_failures", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int32)]),
     ("whit_info_device", _VP, [_VP]),
     ("whit_wbits_detected", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    ("whit_ws_set_twist", ctypes.c_int, [_VP, ctypes.c_int]),
+    ("whit_twist_groups", ctypes.c_int, [_VP, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("whit_ws_bytes_bands", _SZ, [ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     ("whit_ws_create_bands", ctypes.c_int, [ctypes.POINTER(_VP), ctypes.c_int, _I64, _I64, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, _VP, _SZ, _VP]),
@@ -159,6 +161,10 @@ class Workspace:
                    "whit_ws_create_bands")
         self.handle = h
 
+    def set_twist(self, mode: int):
+        """-1 auto, 0 never, 1 whenever the shape allows (whit_ws_set_twist)."""
+        _check(_lib.whit_ws_set_twist(self.handle, int(mode)), "whit_ws_set_twist")
+
     def set_stream(self, stream=None):
         _check(_lib.whit_ws_set_stream(self.handle, _stream_handle(stream)), "whit_ws_set_stream")
 
@@ -276,6 +282,13 @@ def whit_wbits_detected(ws: Workspace):
     nb, nw = ctypes.c_int64(0), ctypes.c_int64(0)
     _check(_lib.whit_wbits_detected(ws.handle, ctypes.byref(nb), ctypes.byref(nw)), "whit_wbits_detected")
     return int(nb.value), int(nw.value)
+
+
+def whit_twist_groups(ws: Workspace):
+    """(groups of 32 series solved on the twisted path, groups) of the last whit_forward (synchronises)."""
+    nt, ng = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(_lib.whit_twist_groups(ws.handle, ctypes.byref(nt), ctypes.byref(ng)), "whit_twist_groups")
+    return int(nt.value), int(ng.value)
 
 
 def whit_host_ws_bytes(d: int, T: int, chunk: int, dtype, per_date: bool, nbuf: int) -> int:

@@ -1,0 +1,12 @@
+// Explicit instantiations: twisted single-series kernels, d = 2 (see whit_launch.cuh).
+#define WHIT_LAUNCH_DEFS
+#include "whit_launch.cuh"
+namespace whit_detail {
+#define WHIT_INST(IO, PD)                                                                  \
+  template whit_status launch_tw<2, IO, PD, false>(const whit::Params&, cudaStream_t); \
+  template whit_status launch_tw<2, IO, PD, true>(const whit::Params&, cudaStream_t);
+WHIT_INST(float, true)
+WHIT_INST(float, false)
+WHIT_INST(double, true)
+WHIT_INST(double, false)
+}  // namespace whit_detail

@@ -54,7 +54,7 @@ static_assert(whit::Tile<float, 1, false>::K == whit::Tile<double, 2, true>::K &
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-  size_t off_dz, off_ckfac, off_ckrf, off_ckrb, off_info, off_cnt, off_wbits, off_wflag, total;
+  size_t off_dz, off_ckfac, off_ckrf, off_ckrb, off_info, off_cnt, off_wbits, off_wflag, off_twflag, total;
 };
 
 // Workspace of nb bands x B pixels: D z cache [nb][T-d][B] (I/O dtype), factor
@@ -66,7 +66,8 @@ bool layout(int d, int64_t T, int64_t B, int nb, whit_dtype dt, WsLayout* L, int
     return false;
   const size_t esz = dt == WHIT_F32 ? 4 : 8;
   if (kk == 0) kk = chunk_k_bands(d, nb);
-  const int64_t C = (T + kk - 1) / kk;
+  // checkpoint slots: ceil(T/K) chunks, +2 for the twisted path's two halves (C1 + C2 <= C + 2)
+  const int64_t C = (T + kk - 1) / kk + 2;
   const int nfac = d + d * (d - 1) / 2;
   size_t o = 0;
   L->off_dz = o;    o = align256(o + size_t(nb) * size_t(T - d) * size_t(B) * esz);
@@ -78,6 +79,7 @@ bool layout(int d, int64_t T, int64_t B, int nb, whit_dtype dt, WsLayout* L, int
   // binary-W detection of the plain forward: the bit plane of W [ceil(T/32)][B] and one flag per warp
   L->off_wbits = o; o = align256(o + size_t((T + 31) / 32) * size_t(B) * 4);
   L->off_wflag = o; o = align256(o + size_t((B + 31) / 32) * 4);
+  L->off_twflag = o; o = align256(o + size_t((B + 31) / 32) * 4);  // twisted path: per warp group
   L->total = o;
   return true;
 }
@@ -153,6 +155,8 @@ struct whit_ws {
   const void* times;
   const uint32_t* wbits;  // bit-packed W of the last forward (whit_forward_wbits), else NULL
   bool wdet;              // the last forward was the plain float-W forward with binary-W detection on
+  bool tw;                // the last forward ran the twisted path (+ its whit_kernel fallback)
+  int tw_mode;            // whit_ws_set_twist: -1 auto (WHIT_TWIST / batch size), 0 never, 1 when the shape allows
   whit_dtype dt;
   whit_lambda_mode lm;
   char* buf;
@@ -209,8 +213,9 @@ struct DeviceGuard {
 // plane or bit-packed), lambda, z, the dates of an irregular grid.  (A stale field -- e.g. the bit
 // plane of an earlier whit_forward_wbits -- would silently steer the next backward.)
 void mark_forward(whit_ws* ws, const void* w, const void* lam, const void* z, const uint32_t* wbits,
-                  const void* times, bool wdet = false) {
+                  const void* times, bool wdet = false, bool tw = false) {
   ws->wdet = wdet;
+  ws->tw = tw;
   ws->have_fwd = true;
   ws->have_info = true;
   ws->w = w;
@@ -381,6 +386,95 @@ whit_status dispatch_irr(const whit_ws* ws, const Params& p) {
             : dispatch_irr_d<double, false, BWD>(ws->d, mb, p, ws->stream);
 }
 
+// ---------------------------------------------------------------- twisted path (whit_twist.cuh)
+// Split row m: a multiple of K near the middle, so the top half runs m + d rows and the bottom T - m.
+int tw_split(const whit_ws* ws) { return ws->kk * int((ws->T - ws->d) / (2 * ws->kk)); }
+
+// Small batches take the twisted path: a warp group's 32 series are split in time between two warps, which
+// halves the per-series latency and doubles the warps in flight where whit_kernel fills the GPU only ~1-2
+// times.  WHIT_TWIST=0 never, =1 whenever the shape allows; default: at most two waves of whit_kernel's
+// 12 warps/SM (B <= 148 * 12 * 32 * 2 series).
+bool tw_pick(const whit_ws* ws) {
+  if (ws->nb != 1 || ws->irr) return false;
+  const int m = tw_split(ws);
+  if (m < ws->kk || ws->T - m - ws->d < ws->kk) return false;  // each half needs a chunk beyond S
+  static const int env_mode = [] {
+    const char* e = std::getenv("WHIT_TWIST");
+    return e ? (e[0] == '0' ? 0 : e[0] == '1' ? 1 : 2) : 2;
+  }();
+  const int mode = ws->tw_mode >= 0 ? ws->tw_mode : env_mode;
+  if (mode == 0) return false;
+  if (mode == 1) return true;
+  return ws->B <= 148LL * 12 * 32 * 2;
+}
+
+// Tensor maps of the two halves (2-D, box K rows; lambda box K + d): top planes cut at row m, bottom planes
+// based at row m.  rhs: y (forward) / grad_z (backward); out0: z / grad_y; out1: the D z cache (forward) /
+// grad_lambda per date (backward); dz: the D z cache (backward).
+whit_status tw_fill(const whit_ws* ws, Params* p, const void* rhs, const void* w, const void* lam, void* out0,
+                    void* out1, const void* dz, bool bwd) {
+  std::memset(p, 0, sizeof *p);
+  const int d = ws->d, K = ws->kk, m = tw_split(ws);
+  const int64_t T = ws->T, B = ws->B;
+  const size_t esz = ws->dt == WHIT_F32 ? 4 : 8;
+  const size_t off = size_t(m) * size_t(B) * esz;  // byte offset of row m in a [rows][B] plane
+  auto at = [&](const void* ptr) { return static_cast<const char*>(ptr) + off; };
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  whit_status st;
+  if ((st = wmap(ws, &p->tm_rhs, rhs, ws->dt, B, m, K)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p->tm_w, w, ws->dt, B, m, K)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p->tmb_rhs, at(rhs), ws->dt, B, T - m, K)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p->tmb_w, at(w), ws->dt, B, T - m, K)) != WHIT_OK) return st;
+  if (pd) {
+    if ((st = wmap(ws, &p->tm_lam_dn, lam, ws->dt, B, m, K + d)) != WHIT_OK) return st;
+    if ((st = wmap(ws, &p->tmb_lam, at(lam), ws->dt, B, T - d - m, K + d)) != WHIT_OK) return st;
+  } else {
+    p->lam_scalar = lam;
+  }
+  if ((st = wmap(ws, &p->tm_out0, out0, ws->dt, B, m, K)) != WHIT_OK) return st;
+  if ((st = wmap(ws, &p->tmb_out0, at(out0), ws->dt, B, T - m, K)) != WHIT_OK) return st;
+  if (!bwd || pd) {
+    if ((st = wmap(ws, &p->tm_out1, out1, ws->dt, B, m, K)) != WHIT_OK) return st;
+    if ((st = wmap(ws, &p->tmb_out1, at(out1), ws->dt, B, T - d - m, K)) != WHIT_OK) return st;
+  }
+  if (bwd) {
+    if ((st = wmap(ws, &p->tm_dz, dz, ws->dt, B, m, K)) != WHIT_OK) return st;
+    if ((st = wmap(ws, &p->tmb_dz, at(dz), ws->dt, B, T - d - m, K)) != WHIT_OK) return st;
+  }
+  p->out1 = out1;  // scalar lambda gradient [B] (backward)
+  p->ck_fac = reinterpret_cast<double*>(ws->buf + ws->L.off_ckfac);
+  p->ck_rhs_f = reinterpret_cast<double*>(ws->buf + ws->L.off_ckrf);
+  p->ck_rhs_b = reinterpret_cast<double*>(ws->buf + ws->L.off_ckrb);
+  p->info = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_info);
+  p->twflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_twflag);
+  p->B = B;
+  p->T = int(T);
+  p->C = int((T + K - 1) / K);
+  p->nb = 1;
+  p->tw_m = m;
+  p->tw_C1 = m / K + 1;
+  p->tw_C2 = int((T - m + K - 1) / K);
+  return WHIT_OK;
+}
+
+template <typename IO, bool PD, bool BWD>
+whit_status dispatch_tw_d(int d, const Params& p, cudaStream_t s) {
+  switch (d) {
+    case 1: return whit_detail::launch_tw<1, IO, PD, BWD>(p, s);
+    case 2: return whit_detail::launch_tw<2, IO, PD, BWD>(p, s);
+    case 3: return whit_detail::launch_tw<3, IO, PD, BWD>(p, s);
+  }
+  return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
+}
+
+template <bool BWD>
+whit_status dispatch_tw(const whit_ws* ws, const Params& p) {
+  const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
+  if (ws->dt == WHIT_F32)
+    return pd ? dispatch_tw_d<float, true, BWD>(ws->d, p, ws->stream) : dispatch_tw_d<float, false, BWD>(ws->d, p, ws->stream);
+  return pd ? dispatch_tw_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_tw_d<double, false, BWD>(ws->d, p, ws->stream);
+}
+
 }  // namespace
 
 extern "C" {
@@ -474,7 +568,8 @@ static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, 
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
-  ws->have_fwd = false; ws->have_info = false; ws->wdet = false; ws->w = ws->lam = ws->z = nullptr;
+  ws->have_fwd = false; ws->have_info = false; ws->wdet = false; ws->tw = false; ws->tw_mode = -1;
+  ws->w = ws->lam = ws->z = nullptr;
   ws->device = -1;
   int dev = -1;
   if (cudaGetDevice(&dev) == cudaSuccess) ws->device = dev;
@@ -517,6 +612,18 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   p.out1 = ws->buf + ws->L.off_dz;
   if ((st = wmap(ws, &p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
   if ((st = wmap(ws, &p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
+  if (C == 1 && tw_pick(ws)) {
+    // twisted kernel, then whit_kernel for the warp groups it handed back (twflag = 0)
+    Params pt;
+    if ((st = tw_fill(ws, &pt, y, w, lambda, z, ws->buf + ws->L.off_dz, nullptr, false)) != WHIT_OK) return st;
+    ws->have_fwd = false;
+    if ((st = dispatch_tw<false>(ws, pt)) != WHIT_OK) return st;
+    p.twflag = pt.twflag;
+    p.tw_filter = 1;
+    if ((st = dispatch<false>(ws, p)) != WHIT_OK) return st;
+    mark_forward(ws, w, lambda, z, nullptr, nullptr, false, true);
+    return WHIT_OK;
+  }
   const bool wdet = C == 1 && wdet_enabled();
   if (wdet) {
     p.wbits_out = reinterpret_cast<uint32_t*>(ws->buf + ws->L.off_wbits);
@@ -683,6 +790,15 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
     p.wbits = ws->wbits;
     return dispatch_wb<true>(ws, p);
   }
+  if (ws->tw) {  // twisted backward, then whit_kernel for the groups the forward handed back
+    Params pt;
+    if ((st = tw_fill(ws, &pt, grad_z, ws->w, ws->lam, grad_y, grad_lambda, ws->buf + ws->L.off_dz, true)) != WHIT_OK)
+      return st;
+    if ((st = dispatch_tw<true>(ws, pt)) != WHIT_OK) return st;
+    p.twflag = pt.twflag;
+    p.tw_filter = 1;
+    return dispatch<true>(ws, p);
+  }
   if (ws->wdet) {  // the forward's binary-W bit plane and per-warp flags (the float plane is read otherwise)
     p.wbits = reinterpret_cast<const uint32_t*>(ws->buf + ws->L.off_wbits);
     p.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
@@ -764,6 +880,36 @@ whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "whit_failures: %s", cudaGetErrorString(e));
   *n_failed = (int64_t)h;
+  return WHIT_OK;
+}
+
+whit_status whit_ws_set_twist(whit_ws* ws, int mode) {
+  if (!ws) return fail(WHIT_ERR_ARG, "ws is NULL");
+  if (mode < -1 || mode > 1) return fail(WHIT_ERR_ARG, "twist mode %d not in {-1, 0, 1}", mode);
+  ws->tw_mode = mode;
+  return WHIT_OK;
+}
+
+whit_status whit_twist_groups(whit_ws* ws, int64_t* n_twisted, int64_t* n_groups) {
+  if (!ws || !n_twisted || !n_groups) return fail(WHIT_ERR_ARG, "NULL argument");
+  if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "no forward has run on this workspace");
+  const long long ng = (ws->B + 31) / 32;
+  *n_groups = ng;
+  *n_twisted = 0;
+  if (!ws->tw) return WHIT_OK;
+  DeviceGuard guard(ws->device);
+  auto* cnt = reinterpret_cast<unsigned long long*>(ws->buf + ws->L.off_cnt);
+  const int32_t* flags = reinterpret_cast<const int32_t*>(ws->buf + ws->L.off_twflag);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof *cnt, ws->stream);
+  if (e == cudaSuccess) {
+    whit::count_failures<<<(unsigned)std::min<long long>((ng + 255) / 256, 4096), 256, 0, ws->stream>>>(flags, ng, cnt);
+    e = cudaGetLastError();
+  }
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, ws->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "whit_twist_groups: %s", cudaGetErrorString(e));
+  *n_twisted = (int64_t)h;
   return WHIT_OK;
 }
 

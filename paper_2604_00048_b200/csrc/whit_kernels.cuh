@@ -74,6 +74,12 @@ struct Params {
   double* ck_rhs_f;       // forward rhs checkpoints [C][nb][d][B]
   double* ck_rhs_b;       // backward rhs checkpoints [C][nb][d][B]
   int32_t* info;          // [B]
+  // twisted factorisation (whit_twist.cuh): maps of the bottom half (planes based at row tw_m), the split row,
+  // the chunk counts of the two halves, per-warp-group decision flags (1: solved twisted; 0: by whit_kernel)
+  CUtensorMap tmb_rhs, tmb_w, tmb_lam, tmb_dz, tmb_out0, tmb_out1;
+  int32_t* twflag;
+  int tw_m, tw_C1, tw_C2;
+  int tw_filter;          // whit_kernel as the twisted path's fallback: skip warp groups with twflag = 1
   long long B;
   int T;
   int C;                  // number of K-step chunks = ceil(T / K)
@@ -656,6 +662,7 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   const int band = 0;
   const long long bw = ((long long)blockIdx.x * L::WARPS + warp) * 32;
   if (bw >= B) return;  // past the end; no barrier follows for these warps
+  if (p.tw_filter && p.twflag[bw >> 5] != 0) return;  // solved by the twisted kernel
   const long long b = bw + lane;
   const bool valid = b < B;
   unsigned char* ring = smem + warp * L::WARP_SMEM;

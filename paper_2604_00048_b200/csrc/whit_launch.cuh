@@ -13,6 +13,7 @@
 #include "whit_internal.h"
 #include "whit_kernels.cuh"
 #include "whit_mb2.cuh"
+#include "whit_twist.cuh"
 
 namespace whit_detail {
 
@@ -32,6 +33,9 @@ whit_status launch_var(const whit::Params& p, cudaStream_t s);
 // Single-series irregular-grid kernel (NEXT-2).
 template <int D, typename IO, bool PD, bool BWD>
 whit_status launch_irr(const whit::Params& p, cudaStream_t s);
+// Twisted (two-ended) single-series kernel for small batches (whit_twist.cuh).
+template <int D, typename IO, bool PD, bool BWD>
+whit_status launch_tw(const whit::Params& p, cudaStream_t s);
 
 #ifdef WHIT_LAUNCH_DEFS
 constexpr int kMaxDevices = 64;
@@ -108,6 +112,18 @@ whit_status launch_irr(const whit::Params& p, cudaStream_t s) {
   const long long per_cta = 32 * L::WARPS;
   const long long grid = (p.B + per_cta - 1) / per_cta;
   K<<<dim3((unsigned)grid), dim3((unsigned)per_cta), L::SMEM, s>>>(p);
+  return launch_error("kernel launch");
+}
+template <int D, typename IO, bool PD, bool BWD>
+whit_status launch_tw(const whit::Params& p, cudaStream_t s) {
+  using L = whit::TwLayout<D, IO, PD, BWD>;
+  static_assert(L::SMEM <= kSmemBudget, "CTA shared memory over budget");
+  constexpr auto K = whit::whit_tw_kernel<D, IO, PD, BWD>;
+  const cudaError_t ae = ensure_smem_attr<K>(L::SMEM);
+  if (ae != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ae));
+  const long long per_cta = 32 * L::PAIRS;  // series per CTA (two warps per 32 series)
+  const long long grid = (p.B + per_cta - 1) / per_cta;
+  K<<<dim3((unsigned)grid), dim3(64 * L::PAIRS), L::SMEM, s>>>(p);
   return launch_error("kernel launch");
 }
 #endif  // WHIT_LAUNCH_DEFS

@@ -58,12 +58,13 @@ def test_ws_bytes(L):
     assert L.whit_ws_bytes(2, 2, 128, 0, 1) == 0
     assert L.whit_ws_bytes(2, 100, 128, 7, 1) == 0
     # holds the D z plane + fp64 checkpoints (5 doubles per series per 16 steps at d = 2, plus the
-    # backward's 2) + info + the binary-W bit plane (1 bit per date) and one flag per warp
+    # backward's 2; two spare chunk slots for the twisted path's halves) + info + the binary-W bit plane
+    # (1 bit per date) and one flag per warp + one twisted-path flag per warp
     T, B = 3288, 262144
     n = P.whit_ws_bytes(2, T, B, torch.float32, True)
     dz = (T - 2) * B * 4
-    ck = ((T + 15) // 16) * (5 + 2) * B * 8
-    bits = ((T + 31) // 32) * B * 4 + (B // 32) * 4
+    ck = ((T + 15) // 16 + 2) * (5 + 2) * B * 8
+    bits = ((T + 31) // 32) * B * 4 + 2 * (B // 32) * 4
     assert dz + ck + 4 * B + bits <= n <= dz + ck + 4 * B + bits + 4096
     assert P.whit_ws_bytes(2, T, B, torch.float64, True) > n
 

@@ -93,12 +93,13 @@ def oracle_info(x, d, times=None):
     return info
 
 
-def check_family(run, x, d, dtype, per_date, times=None, subnormal=None):
+def check_family(run, x, d, dtype, per_date, times=None, subnormal=None, run_ok=None):
     """run(x) -> (dict of output tensors [..., B] or [B], info array).  Checks info against the
-    oracle, NaN in every failed series' outputs, bitwise-unchanged neighbours."""
+    oracle, NaN in every failed series' outputs, bitwise-unchanged neighbours (against run_ok(x) if given,
+    else run(x))."""
     xb, over = inject(x, d, per_date, dtype == torch.float64 if subnormal is None else subnormal)
     out_bad, info = run(xb)
-    out_ok, info_ok = run(x)
+    out_ok, info_ok = (run_ok or run)(x)
     assert np.all(info_ok == 0), info_ok
     ref = oracle_info(xb, d, times)
     bad = sorted(set([B_ZERO, B_NAN, B_NEG, B_NOOBS] + list(over)))

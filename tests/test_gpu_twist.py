@@ -1,0 +1,146 @@
+"""GPU parity of the twisted (two-ended) path for small batches (whit_twist.cuh).
+
+The twisted path is a different elimination order of the same SPD system (Eq. (3)): the top half of
+the dates is factored forward, the bottom half in reversed time, and the two meet in a d x d block.  So it is
+held to the same oracle tolerances as the sequential path (O2 = Algorithm 1 on every series, O1 on a sample),
+on the Sentinel-2 mask (90-day trailing gap) and on iid masks, for z, dL/dy and dL/dlambda (per date and
+scalar), plus: its fallback -- a group whose half is not safely SPD on its own is handed to the sequential
+kernel, whose results it must then equal bit for bit -- and the status rule (every failure case of
+test_gpu_status goes through the fallback, so info is the sequential path's exact row).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import banded as O2
+from oracle import whittaker as O1
+from helpers import check_scalar_lambar, host_inputs, rel_series, ymax_observed
+
+pytestmark = pytest.mark.gpu
+
+TOL = {  # (z, grads) as test_gpu_parity
+    (torch.float32, 1): (1e-4, 1e-3), (torch.float32, 2): (1e-4, 1e-3), (torch.float32, 3): (1e-4, 1e-3),
+    (torch.float64, 1): (1e-10, 1e-9), (torch.float64, 2): (1e-10, 1e-9), (torch.float64, 3): (1e-8, 1e-5),
+}
+
+
+def run(x, d, dtype, twist, T, B):
+    import paper_2604_00048_b200 as P
+    per_date = x["lam"].dim() == 2
+    ws = P.Workspace(d, T, B, dtype, per_date)
+    ws.set_twist(twist)
+    y, w, lam, g = (x[k].to(dtype).contiguous() for k in ("y", "w", "lam", "g"))
+    z, gy, gl = torch.empty_like(y), torch.empty_like(y), torch.empty_like(lam)
+    P.whit_forward(y, w, lam, d, T, B, z, ws)
+    P.whit_backward(g, ws, z, gy, gl)
+    n, info = P.whit_failures(ws, with_info=True)
+    groups = P.whit_twist_groups(ws)
+    torch.cuda.synchronize()
+    return {"z": z, "ybar": gy, "lambar": gl, "info": info, "nfail": n, "groups": groups}
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("T,mask", [(517, "s2"), (3288, "s2"), (700, "bernoulli")])
+def test_twisted_vs_oracle(T, mask, d, per_date, dtype):
+    B = 96
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64, mask=mask,
+                          lam_mode="per_date" if per_date else "scalar", seed=41 + d)
+    r = run(x, d, dtype, 1, T, B)
+    assert r["groups"] == (B // 32, B // 32), r["groups"]  # healthy data: every group twisted
+    assert r["nfail"] == 0
+    h = host_inputs({k: x[k].to(dtype) for k in ("y", "w", "lam", "g")})
+    tz, tg = TOL[(dtype, d)]
+    res = {k: r[k].double().cpu().numpy() for k in ("z", "ybar", "lambar")}
+    res = {k: (v.T if v.ndim == 2 else v) for k, v in res.items()}
+    lam = h["lam"]
+    zr, _, info = O2.forward_banded(h["y"], h["w"], lam, d)
+    yb, lb = O2.backward_banded(h["g"], h["w"], lam, d, zr)
+    if d < 3:  # Algorithm 1 (long double) is the every-series reference where it is fp64-grade
+        ez = rel_series(res["z"], zr, ymax_observed(h["y"], h["w"]))
+        assert ez.max() <= tz, ez.max()
+        assert rel_series(res["ybar"], yb).max() <= tg
+        if per_date:
+            assert rel_series(res["lambar"], lb).max() <= tg
+    for b in (0, 37, 95):  # O1 (dense + refinement)
+        o = O1.forward_backward(h["y"][b], h["w"][b], lam[b], d, h["g"][b])
+        ez = np.max(np.abs(res["z"][b] - o["z"].astype(float))) / ymax_observed(h["y"][b], h["w"][b])
+        assert ez <= tz, (b, ez)
+        assert rel_series(res["ybar"][b], o["ybar"]).max() <= tg, b
+        if per_date:
+            assert rel_series(res["lambar"][b], o["lambar"]).max() <= tg, b
+        else:
+            lam_rep = np.full(T - d, lam[b])
+            _, terms = O2.backward_banded(h["g"][b:b + 1], h["w"][b:b + 1], lam_rep[None, :], d, zr[b:b + 1])
+            check_scalar_lambar(res["lambar"][b], float(o["lambar"]), np.sum(np.abs(terms.astype(float))), tg,
+                                f"twist b={b}")
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_twisted_close_to_sequential(d, dtype):
+    """Same system, two elimination orders: at the homo shape's length the two paths agree far inside the
+    oracle tolerance (both are fp64 deviation-form eliminations)."""
+    T, B = 3288, 64
+    x = synth.make_inputs("homo", B=B, T=T, d=d, device="cuda", dtype=torch.float64)
+    a = run(x, d, dtype, 1, T, B)
+    s = run(x, d, dtype, 0, T, B)
+    assert a["groups"][0] == B // 32 and s["groups"][0] == 0
+    ym = torch.where(x["w"] > 0, x["y"].abs(), torch.zeros_like(x["y"])).amax(0).to(a["z"].device)
+    dz = ((a["z"] - s["z"]).abs().amax(0).double() / ym).max().item()
+    lim = {torch.float32: 1e-6, torch.float64: 1e-10 if d < 3 else 1e-7}[dtype]
+    assert dz <= lim, dz
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+def test_twisted_fallback_group_equals_sequential(per_date, dtype):
+    """A series whose first half has a single observation (its top block is nearly singular): its group of
+    32 goes through the sequential kernel -- bitwise the sequential path's results -- and the other group
+    stays twisted."""
+    d, T, B = 2, 800, 64
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64,
+                          lam_mode="per_date" if per_date else "scalar", mask="bernoulli")
+    x["w"][: T // 2, 40] = 0.0
+    x["w"][5, 40] = 1.0
+    a = run(x, d, dtype, 1, T, B)
+    s = run(x, d, dtype, 0, T, B)
+    assert a["groups"] == (1, 2), a["groups"]
+    for k in ("z", "ybar", "lambar"):
+        assert torch.equal(a[k][..., 32:], s[k][..., 32:]), k
+    tz = TOL[(dtype, d)][0]
+    ym = torch.where(x["w"] > 0, x["y"].abs(), torch.zeros_like(x["y"])).amax(0).to(a["z"].device)
+    assert ((a["z"][:, :32] - s["z"][:, :32]).abs().amax(0).double() / ym[:32]).max().item() <= tz
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_twisted_status_through_fallback(d, per_date, dtype):
+    """The failure cases of test_gpu_status (zero row, NaN lambda, negative lambda, subnormal pivot, no
+    observation) with the twisted path forced: info, NaN outputs and untouched neighbours as there."""
+    import test_gpu_status as S
+    import paper_2604_00048_b200 as P
+
+    def run_mode(xh, mode):
+        xd = S.dev(xh, dtype)
+        ws = P.Workspace(d, S.T_, S.B_, dtype, per_date)
+        ws.set_twist(mode)
+        z, gy, gl = torch.empty_like(xd["y"]), torch.empty_like(xd["y"]), torch.empty_like(xd["lam"])
+        P.whit_forward(xd["y"], xd["w"], xd["lam"], d, S.T_, S.B_, z, ws)
+        P.whit_backward(xd["g"], ws, z, gy, gl)
+        _, info = P.whit_failures(ws, with_info=True)
+        assert P.whit_twist_groups(ws)[0] == (1 if mode == 1 and xh is not x0 else 2 if mode == 1 else 0)
+        return {"z": z.cpu(), "grad_y": gy.cpu(), "grad_lambda": gl.cpu()}, info
+
+    def run_ok(xh):
+        # the failing series sit in group 0, which the bad run hands to the sequential kernel: the healthy
+        # reference is the sequential path there and the twisted path in group 1
+        seq, info = run_mode(xh, 0)
+        tw, _ = run_mode(xh, 1)
+        return {k: torch.cat([seq[k][..., :32], tw[k][..., 32:]], dim=-1) for k in seq}, info
+
+    x0 = S.make_x(d, dtype, per_date)
+    S.check_family(lambda xh: run_mode(xh, 1), x0, d, dtype, per_date, run_ok=run_ok)
