@@ -284,6 +284,7 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
     const bool ok_half = !valid || (bad == 0 && nobs >= 2 * D);
     xme[f * 32 + lane] = ok_half ? 1.0 : 0.0;
   }
+  __syncwarp();  // bar.sync is .aligned: the warp must arrive converged (lane 0 may still be issuing)
   named_bar_sync(pair_bar, 64);
   // both warps: Sigma = Sigma_top + Sigma_bot, r = r_top + r_bot (in that order), LDL^T solve of d x d
   const double* xt = REV ? xother : xme;
@@ -419,6 +420,7 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
   if (lane == 0) bulk_wait0();
   if (BWD && !PD) {  // scalar lambda: dL/dlambda = top rows + bottom rows (in that order)
     if (REV) xme[(L::NX - 1) * 32 + lane] = lam_acc;
+    __syncwarp();
     named_bar_sync(pair_bar, 64);
     if (!REV && valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc + xother[(L::NX - 1) * 32 + lane]);
   }
