@@ -441,7 +441,8 @@ whit_status tw_fill(const whit_ws* ws, Params* p, const void* rhs, const void* w
     if ((st = wmap(ws, &p->tm_dz, dz, ws->dt, B, m, K)) != WHIT_OK) return st;
     if ((st = wmap(ws, &p->tmb_dz, at(dz), ws->dt, B, T - d - m, K)) != WHIT_OK) return st;
   }
-  p->out1 = out1;  // scalar lambda gradient [B] (backward)
+  p->out0 = out0;  // (direct stores of the chunks at S)
+  p->out1 = out1;  // D z / grad_lambda plane, or the scalar lambda gradient [B] (backward)
   p->ck_fac = reinterpret_cast<double*>(ws->buf + ws->L.off_ckfac);
   p->ck_rhs_f = reinterpret_cast<double*>(ws->buf + ws->L.off_ckrf);
   p->ck_rhs_b = reinterpret_cast<double*>(ws->buf + ws->L.off_ckrb);

@@ -47,6 +47,9 @@ struct TwLayout {
   static constexpr uint32_t BYTES = (2 * K + (PD ? K + D : 0) + (BWD ? K : 0)) * ROW;
 };
 
+#ifndef WHIT_TW_STAGE  // debug: stop after stage n (1 init, 2 first tiles, 3 up sweep, 4 exchange); 0 = full
+#define WHIT_TW_STAGE 0
+#endif
 #ifndef WHIT_TW_MAXREG
 #define WHIT_TW_MAXREG 168
 #endif
@@ -209,6 +212,10 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
     for (int s = 0; s < ST && s < ntiles; ++s) tw_issue<D, IO, PD, BWD, REV>(p, ring + s * L::STAGE, &bars[s], s, Cn, (int)bw);
   }
   __syncwarp();
+  if (WHIT_TW_STAGE == 2) {
+    for (int j = 0; j < ST && j < ntiles; ++j) mbar_wait(&bars[j], 0);
+    return;
+  }
   double* const ck_rhs = (BWD ? p.ck_rhs_b : p.ck_rhs_f) + b;
 
   FState<D> st;
@@ -243,6 +250,10 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
     }
   }
 
+  if (WHIT_TW_STAGE == 3) {
+    for (int j = it; j < ntiles && j < it + ST; ++j) mbar_wait(&bars[j % ST], (uint32_t)((j / ST) & 1));
+    return;
+  }
   // ------------------------------------------------------------ the twist: Sigma_x, r_x of this half
   // S index a = date - m.  Top: state row i <-> date m+d-1-i, L_SS lower;  bottom: i <-> date m+i, its
   // reversed-time factor is "upper" in date order.  Sigma_x = L D L^T over S, r_x = L v.
@@ -337,6 +348,10 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
       zS[i] = zz;
     }
   }
+  if (WHIT_TW_STAGE == 4) {
+    for (int j = it; j < ntiles && j < it + ST; ++j) mbar_wait(&bars[j % ST], (uint32_t)((j / ST) & 1));
+    return;
+  }
   if (!BWD) {
     const bool pair_ok = __all_sync(0xffffffffu, ok || !valid);
     if (!pair_ok) {
@@ -397,10 +412,26 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t_lo, m, lam_s, zS, so0 + lane, so1 + lane);
     else
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t_lo, m, lam_s, zS, so0 + lane, so1 + lane);
+    if (edge(c)) {
+      // chunks at S: a tensor store would start outside its plane (top: at row m; bottom: below row m),
+      // so each lane writes its own rows of the staged tile directly, inside the half's rows only
+      IO* o0 = reinterpret_cast<IO*>(p.out0);
+      IO* o1 = reinterpret_cast<IO*>(p.out1);
+      const IO* s0 = so0 + lane;
+      const IO* s1 = so1 + lane;
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) {
+        const int t = t_lo + k, r = REV ? t - D : t;
+        const bool own_t = REV ? (t >= m && t < T) : (t < m);
+        const bool own_r = REV ? (r >= m && r < T - D) : (r < m);
+        if (valid && own_t) o0[(long long)t * B + b] = s0[k * 32];
+        if (valid && (!BWD || PD) && own_r) o1[(long long)r * B + b] = s1[k * 32];
+      }
+    }
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
-      // top maps end at row m (S and beyond are clipped); bottom maps start at row m (rows < m clipped)
+    if (lane == 0 && !edge(c)) {
+      // top maps end at row m; bottom maps start at row m
       if (!REV) {
         tma_store_2d(&p.tm_out0, so0, (int)bw, t_lo);
         if (!BWD || PD) tma_store_2d(&p.tm_out1, so1, (int)bw, t_lo);
@@ -450,6 +481,7 @@ __global__ void __maxnreg__(WHIT_TW_MAXREG) whit_tw_kernel(const __grid_constant
   __syncwarp();
   const double lam_s = (!PD && valid) ? to_f64<IO>(reinterpret_cast<const IO*>(p.lam_scalar)[b]) : 0.0;
   const int pair_bar = 1 + pair;
+  if (WHIT_TW_STAGE == 1) return;
   if (half == 0)
     tw_half<D, IO, PD, BWD, false>(p, ring, bars, xme, xother, pair_bar, lane, bw, valid, b, lam_s);
   else
