@@ -303,8 +303,8 @@ const int32_t* whit_info_device(const whit_ws* ws);
  * per-series latency, twice the warps in flight); a group whose halves are
  * not safely SPD on their own falls back to the sequential kernel inside the
  * same call (results and status as the sequential path).  mode: -1 auto (the
- * default: WHIT_TWIST=0/1 in the environment, else batches of at most two
- * waves, B <= 113,664), 0 never, 1 whenever T allows (T >= about 4K + 2d). */
+ * default: WHIT_TWIST=0/1 in the environment, else B <= 28,416 -- the twisted
+ * warps fit one wave), 0 never, 1 whenever T allows (T >= about 4K + 2d). */
 whit_status whit_ws_set_twist(whit_ws* ws, int mode);
 
 /* SYNCHRONISES the workspace stream, then reports how many groups of 32

@@ -391,9 +391,10 @@ whit_status dispatch_irr(const whit_ws* ws, const Params& p) {
 int tw_split(const whit_ws* ws) { return ws->kk * int((ws->T - ws->d) / (2 * ws->kk)); }
 
 // Small batches take the twisted path: a warp group's 32 series are split in time between two warps, which
-// halves the per-series latency and doubles the warps in flight where whit_kernel fills the GPU only ~1-2
-// times.  WHIT_TWIST=0 never, =1 whenever the shape allows; default: at most two waves of whit_kernel's
-// 12 warps/SM (B <= 148 * 12 * 32 * 2 series).
+// halves the per-series latency and doubles the warps in flight.  It wins while its 2 x B/32 warps fit one
+// wave of 12 warps on each of the 148 SMs (B <= 28,416: 1.85x at B = 8,192, 1.6x at 16,384); beyond that a
+// twisted tail wave costs more than it saves (profiles/r2_twist_sweep.log).  WHIT_TWIST=0 never,
+// =1 whenever the shape allows; whit_ws_set_twist overrides both per workspace.
 bool tw_pick(const whit_ws* ws) {
   if (ws->nb != 1 || ws->irr) return false;
   const int m = tw_split(ws);
@@ -405,7 +406,7 @@ bool tw_pick(const whit_ws* ws) {
   const int mode = ws->tw_mode >= 0 ? ws->tw_mode : env_mode;
   if (mode == 0) return false;
   if (mode == 1) return true;
-  return ws->B <= 148LL * 12 * 32 * 2;
+  return ws->B <= 148LL * 12 * 16;
 }
 
 // Tensor maps of the two halves (2-D, box K rows; lambda box K + d): top planes cut at row m, bottom planes

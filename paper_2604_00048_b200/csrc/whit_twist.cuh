@@ -39,7 +39,11 @@ struct TwLayout {
   static constexpr int OFF_LAM = 2 * K * ROW;                          // (K + d)-row lambda box
   static constexpr int OFF_DZ = OFF_LAM + (PD ? (K + D) * ROW : 0);
   static constexpr int STAGE = (OFF_DZ + (BWD ? K * ROW : 0) + 127) / 128 * 128;
-  static constexpr int OUT = K * ROW;
+#ifndef WHIT_TW_DIRECT  // outputs by direct coalesced stores (no staging planes: 12 warps/SM in both directions)
+#define WHIT_TW_DIRECT 0
+#endif
+  static constexpr bool DIRECT = WHIT_TW_DIRECT;
+  static constexpr int OUT = DIRECT ? 0 : K * ROW;
   static constexpr int NX = D * (D + 1) / 2 + D + 2;                   // exchange fields (fp64) per lane
   static constexpr int XCH = NX * 32 * 8;
   static constexpr int WARP_SMEM = ST * STAGE + 2 * OUT + XCH;
@@ -100,7 +104,8 @@ struct TwSweep {
   template <bool EDGE>
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
                                                     double& lam_acc, const unsigned char* stg, int lane, int t_lo,
-                                                    int m, double lam_s, const double (&zS)[D], IO* so0, IO* so1) {
+                                                    int m, double lam_s, const double (&zS)[D], IO* so0, IO* so1,
+                                                    IO* g0, IO* g1, long long B, bool valid) {
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;
@@ -145,19 +150,30 @@ struct TwSweep {
 #pragma unroll
       for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
       zw[0] = z;
+      IO o0v, o1v = IO(0);
       if (!BWD) {
-        so0[k * 32] = from_f64<IO>(z);
-        so1[k * 32] = from_f64<IO>(dz);
+        o0v = from_f64<IO>(z);
+        o1v = from_f64<IO>(dz);
       } else {
         const double w = to_f64<IO>(t_w[k * 32]);
-        so0[k * 32] = (sizeof(IO) == 4) ? t_w[k * 32] * from_f64<IO>(z) : from_f64<IO>(w * z);
+        o0v = (sizeof(IO) == 4) ? t_w[k * 32] * from_f64<IO>(z) : from_f64<IO>(w * z);
         if (PD) {
-          so1[k * 32] = (sizeof(IO) == 4) ? IO(-(from_f64<IO>(dz) * t_dz[k * 32]))
-                                          : from_f64<IO>(-dz * to_f64<IO>(t_dz[k * 32]));
+          o1v = (sizeof(IO) == 4) ? IO(-(from_f64<IO>(dz) * t_dz[k * 32]))
+                                  : from_f64<IO>(-dz * to_f64<IO>(t_dz[k * 32]));
         } else {
           const bool row_ok = REV ? (t >= m + D) : (t < m);  // this half's difference rows
           if (!EDGE || row_ok) lam_acc += -dz * to_f64<IO>(t_dz[k * 32]);
         }
+      }
+      if (L::DIRECT) {  // this half's rows only: z / grad_y at t, D z / grad_lambda at r (top r = t, bottom t - d)
+        const int r = REV ? t - D : t;
+        const bool own_t = !EDGE || (REV ? t >= m : t < m);
+        const bool own_r = !EDGE || (REV ? r >= m : r < m);
+        if (valid && own_t) g0[(long long)k * B] = o0v;
+        if (valid && (!BWD || PD) && own_r) g1[(long long)k * B] = o1v;
+      } else {
+        so0[k * 32] = o0v;
+        so1[k * 32] = o1v;
       }
     }
 #pragma unroll
@@ -406,13 +422,20 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
       st.lm[i] = l;
       st.id[i] = virt ? 1.0 : rcp64<Newton<IO, D>::N>(l + st.dl[i]);
     }
-    if (lane == 0) bulk_wait_read0();  // staging tiles free again
-    __syncwarp();
+    if (!L::DIRECT) {
+      if (lane == 0) bulk_wait_read0();  // staging tiles free again
+      __syncwarp();
+    }
+    // this chunk's output rows (direct stores): g0 at row t_lo, g1 at row t_lo (top) / t_lo - d (bottom)
+    IO* const g0 = reinterpret_cast<IO*>(p.out0) + b + (long long)t_lo * B;
+    IO* const g1 = reinterpret_cast<IO*>(p.out1) + b + (long long)(REV ? t_lo - D : t_lo) * B;
     if (edge(c))
-      S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t_lo, m, lam_s, zS, so0 + lane, so1 + lane);
+      S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t_lo, m, lam_s, zS, so0 + lane, so1 + lane, g0, g1,
+                                   B, valid);
     else
-      S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t_lo, m, lam_s, zS, so0 + lane, so1 + lane);
-    if (edge(c)) {
+      S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t_lo, m, lam_s, zS, so0 + lane, so1 + lane, g0,
+                                    g1, B, valid);
+    if (!L::DIRECT && edge(c)) {
       // chunks at S: a tensor store would start outside its plane (top: at row m; bottom: below row m),
       // so each lane writes its own rows of the staged tile directly, inside the half's rows only
       IO* o0 = reinterpret_cast<IO*>(p.out0);
@@ -430,7 +453,7 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
     }
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0 && !edge(c)) {
+    if (lane == 0 && !L::DIRECT && !edge(c)) {
       // top maps end at row m; bottom maps start at row m
       if (!REV) {
         tma_store_2d(&p.tm_out0, so0, (int)bw, t_lo);
