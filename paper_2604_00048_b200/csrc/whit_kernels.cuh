@@ -641,44 +641,29 @@ struct Sweep {
 };
 
 // ------------------------------------------------------------------ the kernel
-// One launch = one full forward (BWD=false) or backward (BWD=true) of independent series.  Each
-// warp owns 32 consecutive series (one per lane) and its own TMA ring: up sweep over C chunks,
-// then down sweep over C chunks in reverse; WARPS independent warps per CTA.  (Multi-band
-// pixels sharing a factor use whit_mb2_kernel, whit_mb2.cuh.)
-template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
-__global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid_constant__ Params p) {
-  static_assert(!LOSS || !BWD, "the fused loss is a forward variant");
-  static_assert(!WB || !LOSS, "bit-packed W is a fwd/bwd variant");
+// The kernel body of one warp (32 series).  ring / bars: this warp's smem ring (sized by the launching
+// layout) and mbarriers; ub: W is read as bits (WB, or the binary-W flag of the plain backward).
+template <int D, typename IO, bool PD, bool BWD, bool LOSS, bool WB>
+__device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, uint64_t* bars, int lane,
+                                          long long bw, bool ub) {
   using L = Layout<D, IO, PD, BWD, LOSS, WB>;
   using S = Sweep<D, IO, PD, BWD, LOSS, WB>;
   constexpr int K = L::K, ST = L::ST;
   constexpr int NFAC = Ck<D>::NFAC;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[L::WARPS][ST];
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = p.T, C = p.C, nb = 1;
   const long long B = p.B;
   const int band = 0;
-  const long long bw = ((long long)blockIdx.x * L::WARPS + warp) * 32;
-  if (bw >= B) return;  // past the end; no barrier follows for these warps
-  if (p.tw_filter && p.twflag[bw >> 5] != 0) return;  // solved by the twisted kernel
   const long long b = bw + lane;
   const bool valid = b < B;
-  unsigned char* ring = smem + warp * L::WARP_SMEM;
   IO* so0 = reinterpret_cast<IO*>(ring + ST * L::STAGE);             // output staging
   IO* so1 = reinterpret_cast<IO*>(ring + ST * L::STAGE + L::OUT);
-  uint64_t* bars = full_bar[warp];
   const int ntiles = 2 * C;
 
   // Binary-W detection (WD): the plain forward gathers the mask bits of its series in the up
   // sweep, writes them to the workspace's bit plane and, if all 32 series of the warp have w in {0, 1},
-  // a per-warp flag; from then on its down sweep and both sweeps of the backward read the bits instead of
-  // the float w rows (their TMA loads are skipped).  ub: this warp reads W as bits now.
+  // a per-warp flag; from then on its down sweep reads the bits instead of the float w rows (their TMA loads
+  // are skipped), and the backward of a flagged warp runs this body with WB = true.
   constexpr bool WD = S::WD;
-  constexpr bool WDB = BWD && !WB && !LOSS;
-  bool ub = WB;
-  if (WDB && p.wflag != nullptr) ub = p.wflag[bw >> 5] != 0;
 
   if (lane == 0) {
 #pragma unroll
@@ -868,6 +853,33 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   if (lane == 0) bulk_wait0();  // stores complete before the CTA exits (smem stays valid)
   if (LOSS && valid) reinterpret_cast<IO*>(p.loss)[b] = from_f64<IO>(lam_acc / (double)T);
   if (BWD && !PD && valid) reinterpret_cast<IO*>(p.out1)[b] = from_f64<IO>(lam_acc);
+}
+
+// One launch = one full forward (BWD=false) or backward (BWD=true) of independent series.  Each
+// warp owns 32 consecutive series (one per lane) and its own TMA ring: up sweep over C chunks,
+// then down sweep over C chunks in reverse; WARPS independent warps per CTA.  (Multi-band
+// pixels sharing a factor use whit_mb2_kernel, whit_mb2.cuh.)  The plain backward runs a warp whose
+// forward found W binary with the compile-time bit-packed body (no per-row bit / float select).
+template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
+__global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel(const __grid_constant__ Params p) {
+  static_assert(!LOSS || !BWD, "the fused loss is a forward variant");
+  static_assert(!WB || !LOSS, "bit-packed W is a fwd/bwd variant");
+  using L = Layout<D, IO, PD, BWD, LOSS, WB>;
+  static_assert(!BWD || WB || Layout<D, IO, PD, BWD, LOSS, true>::WARP_SMEM <= L::WARP_SMEM, "bits body ring");
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full_bar[L::WARPS][L::ST];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long bw = ((long long)blockIdx.x * L::WARPS + warp) * 32;
+  if (bw >= p.B) return;  // past the end; no barrier follows for these warps
+  if (p.tw_filter && p.twflag[bw >> 5] != 0) return;  // solved by the twisted kernel
+  unsigned char* ring = smem + warp * L::WARP_SMEM;
+  if constexpr (BWD && !WB && !LOSS) {
+    if (p.wflag != nullptr && p.wflag[bw >> 5] != 0) {
+      whit_body<D, IO, PD, BWD, LOSS, true>(p, ring, full_bar[warp], lane, bw, true);
+      return;
+    }
+  }
+  whit_body<D, IO, PD, BWD, LOSS, WB>(p, ring, full_bar[warp], lane, bw, WB);
 }
 
 // ------------------------------------------------------------------ irregular grid (NEXT-2)
