@@ -544,13 +544,15 @@ struct Sweep {
   // Outputs of row t0+k go to the warp's staging tiles so0/so1 (row k, this
   // lane's column); the caller writes them out with TMA stores, which clip
   // rows past T (z, grad_y) or T-d (D z, grad_lambda) and columns past B.
-  template <bool RAGGED>
+  // UB: W read as bits in this chunk (compile-time: the forward picks the instantiation after its warp vote)
+  template <bool RAGGED, bool UB = WB>
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
                                                     double& lam_acc, const unsigned char* stg, int lane, int t0,
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
                                                     double two_over_T = 0.0, uint32_t wm = 0, IO* gz0 = nullptr,
                                                     long long Bst = 0, bool valid = false, IO* gl0 = nullptr,
-                                                    bool ub = WB) {
+                                                    bool /*unused*/ = WB) {
+    constexpr bool ub = UB;
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -829,12 +831,22 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
                   : L::DIRECT ? reinterpret_cast<IO*>(p.out0) + (long long)t0 * B + b : nullptr;
     IO* const gl0 = ((L::BDIRECT && PD) || L::FDIRECT) ? reinterpret_cast<IO*>(p.out1) + (long long)t0 * B + b
                                                        : nullptr;
-    if (c < cr)
+    // W as bits in the down sweep: WB bodies always; the plain forward once its warp vote found W binary
+    // (a warp-uniform branch between two compile-time instantiations, no per-row bit / float select)
+    if (WD && ub) {
+      if (c < cr)
+        S::template down_chunk<false, true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
+                                            nullptr, two_over_T, wm, gz0, B, valid, gl0);
+      else
+        S::template down_chunk<true, true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
+                                           nullptr, two_over_T, wm, gz0, B, valid, gl0);
+    } else if (c < cr) {
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    nullptr, two_over_T, wm, gz0, B, valid, gl0, ub);
-    else
+                                    nullptr, two_over_T, wm, gz0, B, valid, gl0);
+    } else {
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   nullptr, two_over_T, wm, gz0, B, valid, gl0, ub);
+                                   nullptr, two_over_T, wm, gz0, B, valid, gl0);
+    }
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
     if (lane == 0 && !L::DIRECT) {
