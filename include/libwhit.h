@@ -269,7 +269,9 @@ whit_status whit_forward_wbits(const void* y, const uint32_t* wbits, const void*
  * loss_w [T][B] selects / weights the scored dates (0 = not scored; y may be
  * NaN there).  Same z and factor_ws state as whit_forward: feed grad_z to
  * whit_backward.  Saves the separate loss/gradient pass over z (and the
- * round trip of g).  Single-band workspaces.  One launch. */
+ * round trip of g).  Binary-W detection as in whit_forward (the matching
+ * whit_backward reads W as bits where it is binary).  Single-band workspaces.
+ * One launch. */
 whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, const void* loss_w, int d, int64_t T,
                              int64_t B, void* z, void* grad_z, void* loss, whit_ws* factor_ws);
 

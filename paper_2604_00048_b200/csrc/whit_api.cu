@@ -743,6 +743,12 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
   if ((st = wmap(ws, &p.tm_out2, grad_z, ws->dt, B, T, kK, 1)) != WHIT_OK) return st;
   p.loss = loss;
   p.out2 = grad_z;
+  const bool wdet = wdet_enabled();  // binary-W detection as in whit_forward: the backward reads bits
+  if (wdet) {
+    p.wbits_out = reinterpret_cast<uint32_t*>(ws->buf + ws->L.off_wbits);
+    p.wbits = p.wbits_out;
+    p.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
+  }
   ws->have_fwd = false;
   const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
   if (ws->dt == WHIT_F32)
@@ -750,7 +756,7 @@ whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, c
   else
     st = pd ? dispatch_loss_d<double, true>(d, p, ws->stream) : dispatch_loss_d<double, false>(d, p, ws->stream);
   if (st != WHIT_OK) return st;
-  mark_forward(ws, w, lambda, z, nullptr, nullptr);
+  mark_forward(ws, w, lambda, z, nullptr, nullptr, wdet);
   return WHIT_OK;
 }
 

@@ -467,7 +467,7 @@ struct Sweep {
 
   // ---- up sweep over one chunk (rows t0..t0+K-1); RAGGED: the chunk reaches row T-D or beyond
   // WD (plain forward): also gathers the chunk's mask bits (cb) and whether every w is exactly 0 / 1.
-  static constexpr bool WD = !BWD && !LOSS && !WB;
+  static constexpr bool WD = !BWD && !WB;
   template <bool RAGGED>
   static __device__ __forceinline__ void up_chunk(FState<D>& st, const unsigned char* stg, int lane, int t0, int T,
                                                   double lam_s, int& nobs, bool& pos, uint32_t wm, bool ub,
@@ -551,8 +551,10 @@ struct Sweep {
                                                     int T, double lam_s, IO* so0, IO* so1, IO* so2 = nullptr,
                                                     double two_over_T = 0.0, uint32_t wm = 0, IO* gz0 = nullptr,
                                                     long long Bst = 0, bool valid = false, IO* gl0 = nullptr,
-                                                    bool /*unused*/ = WB) {
-    constexpr bool ub = UB;
+                                                    bool ub_rt = WB) {
+    // UB = true: bits at compile time; otherwise the runtime flag (the plain forward before / without
+    // the compile-time instantiation)
+    const bool ub = UB || ub_rt;
     const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
     const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
@@ -832,8 +834,10 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
     IO* const gl0 = ((L::BDIRECT && PD) || L::FDIRECT) ? reinterpret_cast<IO*>(p.out1) + (long long)t0 * B + b
                                                        : nullptr;
     // W as bits in the down sweep: WB bodies always; the plain forward once its warp vote found W binary
-    // (a warp-uniform branch between two compile-time instantiations, no per-row bit / float select)
-    if (WD && ub) {
+    // (a warp-uniform branch between two compile-time instantiations, no per-row bit / float select:
+    // hetero forward 5.00 vs 5.12 ms).  Per-date lambda only: with scalar lambda the second instantiation
+    // spills at 168 registers (homo forward 1.77 vs 1.65 ms), so there the runtime select stays.
+    if (WD && PD && ub) {
       if (c < cr)
         S::template down_chunk<false, true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
                                             nullptr, two_over_T, wm, gz0, B, valid, gl0);
@@ -842,10 +846,10 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
                                            nullptr, two_over_T, wm, gz0, B, valid, gl0);
     } else if (c < cr) {
       S::template down_chunk<false>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                    nullptr, two_over_T, wm, gz0, B, valid, gl0);
+                                    nullptr, two_over_T, wm, gz0, B, valid, gl0, ub);
     } else {
       S::template down_chunk<true>(st, cA, zw, lam_acc, stg, lane, t0, T, lam_s, so0 + lane, so1 + lane,
-                                   nullptr, two_over_T, wm, gz0, B, valid, gl0);
+                                   nullptr, two_over_T, wm, gz0, B, valid, gl0, ub);
     }
     fence_proxy_async_smem();  // make this lane's staged outputs visible to the TMA engine
     __syncwarp();
