@@ -721,15 +721,18 @@ def run_op(args, P, synth, dev, stream, ws_n, rank):
         gl, loss = torch.empty_like(lam), torch.empty(B, dtype=io, device=dev)
         launches = [("whit_forward_mse", lambda: P.whit_forward_mse(y, w, lam, lw, d, T, B, z, gz, loss, wsp)),
                     ("whit_backward", lambda: P.whit_backward(gz, wsp, z, gy, gl))]
-        fb, bb, _, _ = algorithmic_bytes(B, T, d, esz, per_date)
-        kb = {"whit_forward_mse": fb + loss_fwd_extra_bytes(B, T, esz), "whit_backward": bb}
         metric = "training steps (fused masked-MSE fwd + bwd) series/s"
+        kb = None  # after the timed steps: the byte model of the path that ran (binary W as bits or not)
     else:
         var = torch.empty_like(w)
         launches = [("whit_posterior_variance", lambda: P.whit_posterior_variance(w, lam, d, T, B, var, wsp))]
         kb = {"whit_posterior_variance": variance_bytes(B, T, d, esz, per_date)}
         metric = "posterior variance diag(Omega^-1) series/s"
     ms, per, clocks = timed_steps(launches, args.steps, args.warmup, dev, stream)
+    if kb is None:
+        nbin, nwarps = P.whit_wbits_detected(wsp)
+        fb, bb, _, _ = algorithmic_bytes(B, T, d, esz, per_date, wdet=(nbin == nwarps and nwarps > 0))
+        kb = {"whit_forward_mse": fb + loss_fwd_extra_bytes(B, T, esz), "whit_backward": bb}
     if rank == 0:
         print(json.dumps(base_line(
             args, metric, ws_n * B / (ms / 1e3), UNIT, ws_n, ms, len(launches) * args.steps,
