@@ -357,6 +357,12 @@ template <int D> struct Ck {
 #ifndef WHIT_TILE_ST
 #define WHIT_TILE_ST 2
 #endif
+#ifndef WHIT_BWD_WB_ST
+#define WHIT_BWD_WB_ST 2
+#endif
+#ifndef WHIT_BWD_WB_DIRECT
+#define WHIT_BWD_WB_DIRECT 0
+#endif
 #ifndef WHIT_FWD_WARPS
 #define WHIT_FWD_WARPS 4
 #endif
@@ -373,7 +379,9 @@ constexpr int kMaxBands = 10;
 
 template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false> struct Layout {
   // LOSS: 2-warp CTAs (its stage carries the loss weights too: 10 warps/SM fit at <= 200 registers)
-  static constexpr int K = Tile<IO, D, BWD>::K, ST = Tile<IO, D, BWD>::ST,
+  // the bit-packed backward body (WB) may run a deeper ring (WHIT_BWD_WB_ST): without the w rows its stages are
+  // smaller, and it runs inside the float layout's per-warp allocation when it serves the plain backward
+  static constexpr int K = Tile<IO, D, BWD>::K, ST = (BWD && WB) ? WHIT_BWD_WB_ST : Tile<IO, D, BWD>::ST,
                        WARPS = LOSS ? 2 : Tile<IO, D, BWD>::WARPS;
   static constexpr int ROW = 32 * (int)sizeof(IO);  // bytes of one staged time row (one warp)
   static constexpr int OFF_RHS = 0;
@@ -387,7 +395,7 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   // and direct 128-B warp stores, were measured no faster: DESIGN.md §5)
   // backward outputs by direct coalesced stores (WHIT_BWD_DIRECT): no staging planes, 10 warps/SM
   // (measured +2% backward on homo/hetero; the bit-W backward stays staged: direct was 8% slower there)
-  static constexpr bool BDIRECT = BWD && !WB && WHIT_BWD_DIRECT;
+  static constexpr bool BDIRECT = BWD && (WB ? WHIT_BWD_WB_DIRECT : WHIT_BWD_DIRECT);
   // plain forward: z and D z by direct coalesced stores too (WHIT_FWD_DIRECT)
   static constexpr bool FDIRECT = !BWD && !WB && !LOSS && WHIT_FWD_DIRECT;
   static constexpr bool DIRECT = BDIRECT || FDIRECT;
@@ -883,7 +891,9 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   using L = Layout<D, IO, PD, BWD, LOSS, WB>;
   static_assert(!BWD || WB || Layout<D, IO, PD, BWD, LOSS, true>::WARP_SMEM <= L::WARP_SMEM, "bits body ring");
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t full_bar[L::WARPS][L::ST];
+  // mbarriers: enough for the bit-packed backward body's ring too (WHIT_BWD_WB_ST)
+  constexpr int NBAR = Layout<D, IO, PD, BWD, LOSS, true>::ST > L::ST ? Layout<D, IO, PD, BWD, LOSS, true>::ST : L::ST;
+  __shared__ __align__(8) uint64_t full_bar[L::WARPS][NBAR];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long bw = ((long long)blockIdx.x * L::WARPS + warp) * 32;
   if (bw >= p.B) return;  // past the end; no barrier follows for these warps
