@@ -304,9 +304,14 @@ const int32_t* whit_info_device(const whit_ws* ws);
  * second half in reversed time; they meet in a d x d block -- half the
  * per-series latency, twice the warps in flight); a group whose halves are
  * not safely SPD on their own falls back to the sequential kernel inside the
- * same call (results and status as the sequential path).  mode: -1 auto (the
- * default: WHIT_TWIST=0/1 in the environment, else B <= 28,416 -- the twisted
- * warps fit one wave), 0 never, 1 whenever T allows (T >= about 4K + 2d). */
+ * same call (results and status as the sequential path).  Batches just past
+ * one wave of the sequential kernel (1,776 < ceil(B/32) <= 2,400 groups, e.g.
+ * B = 65,536) take a HYBRID launch: the first 1,632 groups sequential, the
+ * rest twisted on a second stream (forked and joined with events on the
+ * workspace stream).  mode: -1 auto (the default: WHIT_TWIST=0/1 in the
+ * environment, else twisted for B <= 28,416 -- its warps fit one wave -- and
+ * hybrid as above; WHIT_HYBRID=0 turns the hybrid off), 0 never, 1 twisted
+ * whenever T allows (T >= about 4K + 2d), 2 hybrid whenever B > 1,632 * 32. */
 whit_status whit_ws_set_twist(whit_ws* ws, int mode);
 
 /* SYNCHRONISES the workspace stream, then reports how many groups of 32

@@ -157,6 +157,9 @@ struct whit_ws {
   bool wdet;              // the last forward was the plain float-W forward with binary-W detection on
   bool tw;                // the last forward ran the twisted path (+ its whit_kernel fallback)
   int tw_mode;            // whit_ws_set_twist: -1 auto (WHIT_TWIST / batch size), 0 never, 1 when the shape allows
+  int hyb_g1;             // hybrid launch of the last forward: groups [0, g1) sequential, [g1, G) twisted (0: none)
+  cudaStream_t aux = nullptr;            // hybrid launch: the twisted part's stream (created on first use)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   whit_dtype dt;
   whit_lambda_mode lm;
   char* buf;
@@ -213,9 +216,10 @@ struct DeviceGuard {
 // plane or bit-packed), lambda, z, the dates of an irregular grid.  (A stale field -- e.g. the bit
 // plane of an earlier whit_forward_wbits -- would silently steer the next backward.)
 void mark_forward(whit_ws* ws, const void* w, const void* lam, const void* z, const uint32_t* wbits,
-                  const void* times, bool wdet = false, bool tw = false) {
+                  const void* times, bool wdet = false, bool tw = false, int hyb_g1 = 0) {
   ws->wdet = wdet;
   ws->tw = tw;
+  ws->hyb_g1 = hyb_g1;
   ws->have_fwd = true;
   ws->have_info = true;
   ws->w = w;
@@ -403,10 +407,41 @@ bool tw_pick(const whit_ws* ws) {
     const char* e = std::getenv("WHIT_TWIST");
     return e ? (e[0] == '0' ? 0 : e[0] == '1' ? 1 : 2) : 2;
   }();
-  const int mode = ws->tw_mode >= 0 ? ws->tw_mode : env_mode;
+  const int mode = ws->tw_mode == 2 ? 0 : ws->tw_mode >= 0 ? ws->tw_mode : env_mode;
   if (mode == 0) return false;
   if (mode == 1) return true;
   return ws->B <= 148LL * 12 * 16;
+}
+
+// Hybrid launch for batches just past one wave of whit_kernel (1,776 < G <= 2,400 groups of 32, e.g. homo's
+// 2,048): the first kHybG1 groups run the sequential kernel (its wave) while the remaining groups run twisted
+// on a second stream, filling the slots the first wave leaves and finishing the tail in half the latency
+// (homo 22.6 -> 23.9 M series/s in the two-stream probe, tools/kdev/hybrid_probe.py).  Auto mode only.
+constexpr int kHybG1 = 1632;  // even (two groups per twisted CTA); 144 of the 1,776 slots left to the twisted part
+int hyb_pick(const whit_ws* ws) {
+  if (ws->nb != 1 || ws->irr) return 0;
+  if (ws->tw_mode == 2) {  // forced (tests): whenever there are groups beyond kHybG1
+    const int m = tw_split(ws);
+    return (m >= ws->kk && ws->T - m - ws->d >= ws->kk && (ws->B + 31) / 32 > kHybG1) ? kHybG1 : 0;
+  }
+  if (ws->tw_mode >= 0) return 0;
+  const char* e = std::getenv("WHIT_TWIST");
+  if (e && (e[0] == '0' || e[0] == '1')) return 0;
+  const char* h = std::getenv("WHIT_HYBRID");
+  if (h && h[0] == '0') return 0;
+  const int m = tw_split(ws);
+  if (m < ws->kk || ws->T - m - ws->d < ws->kk) return 0;
+  const long long G = (ws->B + 31) / 32;
+  return (G > 148 * 12 && G <= 2400) ? kHybG1 : 0;
+}
+
+whit_status hyb_streams(whit_ws* ws) {
+  if (ws->aux) return WHIT_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&ws->aux, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_join, cudaEventDisableTiming);
+  if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid launch streams: %s", cudaGetErrorString(e));
+  return WHIT_OK;
 }
 
 // Tensor maps of the two halves (2-D, box K rows; lambda box K + d): top planes cut at row m, bottom planes
@@ -570,7 +605,7 @@ static whit_status ws_create(whit_ws** out, int d, int64_t T, int64_t B, int C, 
   ws->buf = static_cast<char*>(dev_buf); ws->bytes = dev_bytes;
   ws->stream = static_cast<cudaStream_t>(cuda_stream);
   ws->L = L;
-  ws->have_fwd = false; ws->have_info = false; ws->wdet = false; ws->tw = false; ws->tw_mode = -1;
+  ws->have_fwd = false; ws->have_info = false; ws->wdet = false; ws->tw = false; ws->tw_mode = -1; ws->hyb_g1 = 0;
   ws->w = ws->lam = ws->z = nullptr;
   ws->device = -1;
   int dev = -1;
@@ -591,7 +626,16 @@ whit_status whit_ws_set_stream(whit_ws* ws, void* cuda_stream) {
   return WHIT_OK;
 }
 
-void whit_ws_destroy(whit_ws* ws) { delete ws; }
+void whit_ws_destroy(whit_ws* ws) {
+  if (!ws) return;
+  if (ws->aux) {
+    DeviceGuard guard(ws->device);
+    cudaStreamDestroy(ws->aux);
+    cudaEventDestroy(ws->ev_fork);
+    cudaEventDestroy(ws->ev_join);
+  }
+  delete ws;
+}
 
 whit_status whit_forward_bands(const void* y, const void* w, const void* lambda, int d, int64_t T, int64_t B, int C,
                                void* z, whit_ws* ws) {
@@ -614,6 +658,45 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
   p.out1 = ws->buf + ws->L.off_dz;
   if ((st = wmap(ws, &p.tm_out0, z, ws->dt, B, T, kK, C)) != WHIT_OK) return st;
   if ((st = wmap(ws, &p.tm_out1, ws->buf + ws->L.off_dz, ws->dt, B, T - d, kK, C)) != WHIT_OK) return st;
+  if (const int g1 = C == 1 ? hyb_pick(ws) : 0) {
+    // hybrid: groups [0, g1) by whit_kernel on the workspace stream (binary-W detection on), groups [g1, G) by
+    // the twisted kernel + its whit_kernel fallback on the auxiliary stream, forked and joined by events
+    if ((st = hyb_streams(ws)) != WHIT_OK) return st;
+    Params pt;
+    if ((st = tw_fill(ws, &pt, y, w, lambda, z, ws->buf + ws->L.off_dz, nullptr, false)) != WHIT_OK) return st;
+    pt.tw_cta0 = g1 / 2;
+    const bool wdet = wdet_enabled();
+    Params ps = p;
+    ps.g_hi = g1;
+    if (wdet) {
+      ps.wbits_out = reinterpret_cast<uint32_t*>(ws->buf + ws->L.off_wbits);
+      ps.wbits = ps.wbits_out;
+      ps.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
+    }
+    p.twflag = pt.twflag;  // the fallback: whit_kernel over groups [g1, G) the twisted kernel handed back
+    p.tw_filter = 1;
+    ws->have_fwd = false;
+    cudaStream_t main = ws->stream;
+    cudaError_t e = cudaEventRecord(ws->ev_fork, main);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
+    const long long G = (B + 31) / 32;
+    if (e == cudaSuccess)  // groups [0, g1) count as solved for the fallback's filter; no stale W flags above g1
+      e = cudaMemsetAsync(pt.twflag, 0x01, size_t(g1) * 4, ws->aux);
+    if (e == cudaSuccess)
+      e = cudaMemsetAsync(ws->buf + ws->L.off_wflag + size_t(g1) * 4, 0, size_t(G - g1) * 4, ws->aux);
+    if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid fork: %s", cudaGetErrorString(e));
+    if ((st = dispatch<false>(ws, ps)) != WHIT_OK) return st;
+    ws->stream = ws->aux;
+    st = dispatch_tw<false>(ws, pt);
+    if (st == WHIT_OK) st = dispatch<false>(ws, p);
+    ws->stream = main;
+    if (st != WHIT_OK) return st;
+    e = cudaEventRecord(ws->ev_join, ws->aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ws->ev_join, 0);
+    if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid join: %s", cudaGetErrorString(e));
+    mark_forward(ws, w, lambda, z, nullptr, nullptr, wdet, true, g1);
+    return WHIT_OK;
+  }
   if (C == 1 && tw_pick(ws)) {
     // twisted kernel, then whit_kernel for the warp groups it handed back (twflag = 0)
     Params pt;
@@ -798,6 +881,35 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
     p.wbits = ws->wbits;
     return dispatch_wb<true>(ws, p);
   }
+  if (ws->tw && ws->hyb_g1 > 0) {  // hybrid: as the forward split its groups
+    const int g1 = ws->hyb_g1;
+    Params pt;
+    if ((st = tw_fill(ws, &pt, grad_z, ws->w, ws->lam, grad_y, grad_lambda, ws->buf + ws->L.off_dz, true)) != WHIT_OK)
+      return st;
+    pt.tw_cta0 = g1 / 2;
+    Params ps = p;
+    ps.g_hi = g1;
+    if (ws->wdet) {
+      ps.wbits = reinterpret_cast<const uint32_t*>(ws->buf + ws->L.off_wbits);
+      ps.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
+    }
+    p.twflag = pt.twflag;
+    p.tw_filter = 1;
+    cudaStream_t main = ws->stream;
+    cudaError_t e = cudaEventRecord(ws->ev_fork, main);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
+    if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid fork: %s", cudaGetErrorString(e));
+    if ((st = dispatch<true>(ws, ps)) != WHIT_OK) return st;
+    ws->stream = ws->aux;
+    st = dispatch_tw<true>(ws, pt);
+    if (st == WHIT_OK) st = dispatch<true>(ws, p);
+    ws->stream = main;
+    if (st != WHIT_OK) return st;
+    e = cudaEventRecord(ws->ev_join, ws->aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ws->ev_join, 0);
+    if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid join: %s", cudaGetErrorString(e));
+    return WHIT_OK;
+  }
   if (ws->tw) {  // twisted backward, then whit_kernel for the groups the forward handed back
     Params pt;
     if ((st = tw_fill(ws, &pt, grad_z, ws->w, ws->lam, grad_y, grad_lambda, ws->buf + ws->L.off_dz, true)) != WHIT_OK)
@@ -893,7 +1005,7 @@ whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info) {
 
 whit_status whit_ws_set_twist(whit_ws* ws, int mode) {
   if (!ws) return fail(WHIT_ERR_ARG, "ws is NULL");
-  if (mode < -1 || mode > 1) return fail(WHIT_ERR_ARG, "twist mode %d not in {-1, 0, 1}", mode);
+  if (mode < -1 || mode > 2) return fail(WHIT_ERR_ARG, "twist mode %d not in {-1, 0, 1, 2}", mode);
   ws->tw_mode = mode;
   return WHIT_OK;
 }
@@ -917,7 +1029,7 @@ whit_status whit_twist_groups(whit_ws* ws, int64_t* n_twisted, int64_t* n_groups
   if (e == cudaSuccess) e = cudaMemcpyAsync(&h, cnt, sizeof h, cudaMemcpyDeviceToHost, ws->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ws->stream);
   if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "whit_twist_groups: %s", cudaGetErrorString(e));
-  *n_twisted = (int64_t)h;
+  *n_twisted = (int64_t)h - ws->hyb_g1;  // (hybrid: groups [0, g1) are marked solved for the fallback's filter)
   return WHIT_OK;
 }
 

@@ -80,6 +80,8 @@ struct Params {
   int32_t* twflag;
   int tw_m, tw_C1, tw_C2;
   int tw_filter;          // whit_kernel as the twisted path's fallback: skip warp groups with twflag = 1
+  int g_hi;               // hybrid launch (> 0): whit_kernel solves only warp groups [0, g_hi)
+  int tw_cta0;            // hybrid launch: the twisted kernel's first CTA (its groups start at 2 * tw_cta0)
   long long B;
   int T;
   int C;                  // number of K-step chunks = ceil(T / K)
@@ -897,6 +899,7 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long bw = ((long long)blockIdx.x * L::WARPS + warp) * 32;
   if (bw >= p.B) return;  // past the end; no barrier follows for these warps
+  if (p.g_hi > 0 && (bw >> 5) >= p.g_hi) return;       // hybrid: the twisted kernel's groups
   if (p.tw_filter && p.twflag[bw >> 5] != 0) return;  // solved by the twisted kernel
   unsigned char* ring = smem + warp * L::WARP_SMEM;
   if constexpr (BWD && !WB && !LOSS) {

@@ -69,9 +69,10 @@ whit_status launch(const whit::Params& p, cudaStream_t s) {
   constexpr auto K = whit::whit_kernel<D, IO, PD, BWD, LOSS, WB>;
   const cudaError_t ae = ensure_smem_attr<K>(L::SMEM);
   if (ae != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ae));
-  // one series per thread, one TMA pipeline per warp
+  // one series per thread, one TMA pipeline per warp (hybrid: only the CTAs of groups [0, g_hi))
   const int threads = 32 * L::WARPS;
-  const long long grid = (p.B + threads - 1) / threads;
+  const long long nser = p.g_hi > 0 && 32LL * p.g_hi < p.B ? 32LL * p.g_hi : p.B;
+  const long long grid = (nser + threads - 1) / threads;
   K<<<dim3((unsigned)grid), dim3(threads), L::SMEM, s>>>(p);
   return launch_error("kernel launch");
 }
@@ -122,7 +123,7 @@ whit_status launch_tw(const whit::Params& p, cudaStream_t s) {
   const cudaError_t ae = ensure_smem_attr<K>(L::SMEM);
   if (ae != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ae));
   const long long per_cta = 32 * L::PAIRS;  // series per CTA (two warps per 32 series)
-  const long long grid = (p.B + per_cta - 1) / per_cta;
+  const long long grid = (p.B + per_cta - 1) / per_cta - p.tw_cta0;  // (hybrid: from CTA tw_cta0 on)
   K<<<dim3((unsigned)grid), dim3(64 * L::PAIRS), L::SMEM, s>>>(p);
   return launch_error("kernel launch");
 }

@@ -488,7 +488,7 @@ __global__ void __maxnreg__(WHIT_TW_MAXREG) whit_tw_kernel(const __grid_constant
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, half = warp & 1;  // half 0: top, 1: bottom
   const long long B = p.B;
-  const long long bw = ((long long)blockIdx.x * L::PAIRS + pair) * 32;
+  const long long bw = ((long long)(blockIdx.x + p.tw_cta0) * L::PAIRS + pair) * 32;
   if (bw >= B) return;  // both warps of the pair leave together (no barrier is pending)
   const long long b = bw + lane;
   const bool valid = b < B;

@@ -152,3 +152,37 @@ def test_twisted_status_through_fallback(d, per_date, dtype):
 
     x0 = S.make_x(d, dtype, per_date)
     S.check_family(lambda xh: run_mode(xh, 1), x0, d, dtype, per_date, run_ok=run_ok)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+def test_hybrid_launch(per_date, dtype):
+    """Hybrid launch (B just past one wave): groups [0, 1632) by the sequential kernel on the workspace
+    stream, the rest twisted on a second stream.  The sequential part equals the sequential path bitwise;
+    the twisted part agrees with it inside the oracle tolerance (and a failing series there still gets its
+    exact status through the fallback); O1 on a sample of both parts."""
+    d, T, B = 2, 240, 65536
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64, mask="bernoulli",
+                          lam_mode="per_date" if per_date else "scalar", seed=77)
+    if per_date:
+        x["lam"][61, 60000] = float("nan")  # a failing series in the twisted part: info 62
+    a = run(x, d, dtype, 2, T, B)
+    s = run(x, d, dtype, 0, T, B)
+    G1 = 1632 * 32
+    assert a["groups"][1] == B // 32 and a["groups"][0] >= (B - G1) // 32 - 1, a["groups"]
+    for k in ("z", "ybar", "lambar"):
+        assert torch.equal(a[k][..., :G1].nan_to_num(7.0), s[k][..., :G1].nan_to_num(7.0)), k
+    assert np.array_equal(a["info"], s["info"])
+    if per_date:
+        assert a["info"][60000] == 62 and torch.isnan(a["z"][:, 60000]).all()
+    ok = torch.isfinite(a["z"]).all(0)
+    ym = torch.where(x["w"] > 0, x["y"].abs(), torch.zeros_like(x["y"])).amax(0).to(a["z"].device)
+    ez = ((a["z"] - s["z"]).abs().amax(0).double() / ym)[ok].max().item()
+    assert ez <= TOL[(dtype, d)][0], ez
+    h = host_inputs({k: x[k].to(dtype) for k in ("y", "w", "lam", "g")})
+    tz, tg = TOL[(dtype, d)]
+    for b in (5, G1 - 1, G1, B - 1):
+        o = O1.forward_backward(h["y"][b], h["w"][b], h["lam"][b], d, h["g"][b])
+        z = a["z"][:, b].double().cpu().numpy()
+        assert np.max(np.abs(z - o["z"].astype(float))) / ymax_observed(h["y"][b], h["w"][b]) <= tz, b
+        assert rel_series(a["ybar"][:, b].double().cpu().numpy(), o["ybar"]).max() <= tg, b
