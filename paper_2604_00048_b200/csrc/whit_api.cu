@@ -881,34 +881,17 @@ whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* 
     p.wbits = ws->wbits;
     return dispatch_wb<true>(ws, p);
   }
-  if (ws->tw && ws->hyb_g1 > 0) {  // hybrid: as the forward split its groups
-    const int g1 = ws->hyb_g1;
-    Params pt;
-    if ((st = tw_fill(ws, &pt, grad_z, ws->w, ws->lam, grad_y, grad_lambda, ws->buf + ws->L.off_dz, true)) != WHIT_OK)
-      return st;
-    pt.tw_cta0 = g1 / 2;
-    Params ps = p;
-    ps.g_hi = g1;
+  if (ws->tw && ws->hyb_g1 > 0) {
+    // hybrid forward: the backward is ONE sequential launch (its bit-packed body where the forward's sequential
+    // part found W binary); the groups the forward solved twisted rebuild the sequential factor checkpoints in
+    // their up sweep (bwd_fac_from), which that launch's down sweep then reads (measured: the twisted backward
+    // is slower than the sequential one at this size)
+    p.bwd_fac_from = ws->hyb_g1;
     if (ws->wdet) {
-      ps.wbits = reinterpret_cast<const uint32_t*>(ws->buf + ws->L.off_wbits);
-      ps.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
+      p.wbits = reinterpret_cast<const uint32_t*>(ws->buf + ws->L.off_wbits);
+      p.wflag = reinterpret_cast<int32_t*>(ws->buf + ws->L.off_wflag);
     }
-    p.twflag = pt.twflag;
-    p.tw_filter = 1;
-    cudaStream_t main = ws->stream;
-    cudaError_t e = cudaEventRecord(ws->ev_fork, main);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(ws->aux, ws->ev_fork, 0);
-    if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid fork: %s", cudaGetErrorString(e));
-    if ((st = dispatch<true>(ws, ps)) != WHIT_OK) return st;
-    ws->stream = ws->aux;
-    st = dispatch_tw<true>(ws, pt);
-    if (st == WHIT_OK) st = dispatch<true>(ws, p);
-    ws->stream = main;
-    if (st != WHIT_OK) return st;
-    e = cudaEventRecord(ws->ev_join, ws->aux);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ws->ev_join, 0);
-    if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid join: %s", cudaGetErrorString(e));
-    return WHIT_OK;
+    return dispatch<true>(ws, p);
   }
   if (ws->tw) {  // twisted backward, then whit_kernel for the groups the forward handed back
     Params pt;

@@ -82,6 +82,8 @@ struct Params {
   int tw_filter;          // whit_kernel as the twisted path's fallback: skip warp groups with twflag = 1
   int g_hi;               // hybrid launch (> 0): whit_kernel solves only warp groups [0, g_hi)
   int tw_cta0;            // hybrid launch: the twisted kernel's first CTA (its groups start at 2 * tw_cta0)
+  int bwd_fac_from;       // hybrid backward (> 0): groups >= this write the factor checkpoints in the up sweep
+                          // (their forward ran twisted, with its own checkpoint layout)
   long long B;
   int T;
   int C;                  // number of K-step chunks = ceil(T / K)
@@ -722,7 +724,7 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
     const unsigned char* stg = ring + s * L::STAGE;
     const int t0 = c * K;
     if (valid) {  // checkpoint: state entering row t0
-      if (!BWD) {
+      if (!BWD || (p.bwd_fac_from > 0 && (bw >> 5) >= p.bwd_fac_from)) {
         double* ck = p.ck_fac + (long long)c * NFAC * B + b;
         int f = 0;
 #pragma unroll
