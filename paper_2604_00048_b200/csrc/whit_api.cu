@@ -429,10 +429,11 @@ int hyb_pick(const whit_ws* ws) {
   if (e && (e[0] == '0' || e[0] == '1')) return 0;
   const char* h = std::getenv("WHIT_HYBRID");
   if (h && h[0] == '0') return 0;
+  const int hmax = (h && h[0] >= '2' && h[0] <= '9') ? 1 << 30 : 2400;  // WHIT_HYBRID=2: any G > 1,776 (A/B)
   const int m = tw_split(ws);
   if (m < ws->kk || ws->T - m - ws->d < ws->kk) return 0;
   const long long G = (ws->B + 31) / 32;
-  return (G > 148 * 12 && G <= 2400) ? kHybG1 : 0;
+  return (G > 148 * 12 && G <= hmax) ? kHybG1 : 0;
 }
 
 whit_status hyb_streams(whit_ws* ws) {
