@@ -644,12 +644,18 @@ def run_fwdbwd(args, P, synth, dev, stream, ws_n, rank):
     nbin, nwarps = P.whit_wbits_detected(wsp)  # warps of the last forward that read W as bits
     wdet = nbin == nwarps and nwarps > 0
     fb, bb, mf, mb = algorithmic_bytes(B, T, d, esz, per_date, wdet=wdet)
+    if 0 < nbin < nwarps:  # mixed (hybrid launch: its twisted part reads the float W): weight the two models
+        f1, b1, _, _ = algorithmic_bytes(B, T, d, esz, per_date, wdet=True)
+        fr = nbin / nwarps
+        fb, bb = fr * f1 + (1 - fr) * fb, fr * b1 + (1 - fr) * bb
     kb = {"whit_forward": fb} if fwd_only else {"whit_forward": fb, "whit_backward": bb}
     mins = {"whit_forward": mf} if fwd_only else {"whit_forward": mf, "whit_backward": mb}
     dom = max(per, key=per.get)
     roof = roofline(kb, per, ms_step, mins, traffic=profile_fields(dom) if args.config == "hetero" else None,
                     extra={"byte_model": "R-mode, binary-W bit plane detected in the forward" if wdet
-                           else "R-mode, float W plane"})
+                           else ("R-mode, %d of %d warps with W as bits (hybrid / twisted launch)" % (nbin, nwarps)
+                                 if nbin else "R-mode, float W plane")})
+    tw_groups = P.whit_twist_groups(wsp)
 
     # the same step with the binary W bit-packed by the caller (whit_forward_wbits), beside the headline
     wbits_line = None
@@ -694,6 +700,8 @@ def run_fwdbwd(args, P, synth, dev, stream, ws_n, rank):
                          w_bits=wbits_line, e2e_wbits=e2e_wbits, checksums=checksums)
         line["binary_w"] = {"warps_reading_bits": nbin, "warps": nwarps,
                             "how": "whit_forward detected W in {0, 1} per warp of 32 series (DESIGN §5)"}
+        line["path"] = {"twisted_groups": tw_groups[0], "groups": tw_groups[1],
+                        "how": "small batches: twisted factorisation; just past one wave: hybrid launch (DESIGN §5)"}
         print(json.dumps(line), flush=True)
     return 0
 
