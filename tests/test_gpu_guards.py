@@ -82,6 +82,10 @@ def _family_runs(family, d, dtype, per_date, T, B, C=3):
         kw = {"C": C} if bands else {}
         nbytes = P.Workspace(d, T, B, dtype, per_date, times=times, **kw).nbytes
         ws = P.Workspace(d, T, B, dtype, per_date, times=times, buf=G.ws_buf(nbytes) if guarded else None, **kw)
+        if family == "twisted":
+            ws.set_twist(1)
+        elif family == "hybrid":
+            ws.set_twist(2)
         out = {}
         if family == "variance":
             var = go(x["w"])
@@ -89,7 +93,7 @@ def _family_runs(family, d, dtype, per_date, T, B, C=3):
             out["var"] = var
         else:
             z, gy, gl = go(x["y"]), go(x["y"]), go(x["lam"])
-            if family in ("binary", "soft"):
+            if family in ("binary", "soft", "twisted", "hybrid"):
                 P.whit_forward(y, w, lam, d, T, B, z, ws)
             elif family == "wbits":
                 bits = gi(P.whit_pack_mask(x["w"]).contiguous())
@@ -118,7 +122,7 @@ def _family_runs(family, d, dtype, per_date, T, B, C=3):
     return run
 
 
-FAMILIES = ["binary", "soft", "wbits", "mse", "times", "variance", "bands", "bands_times"]
+FAMILIES = ["binary", "soft", "wbits", "mse", "times", "variance", "bands", "bands_times", "twisted"]
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
@@ -137,3 +141,18 @@ def test_guard_bands_and_determinism(family, d, per_date, dtype):
         assert torch.equal(ref[k].nan_to_num(nan=7.0), got[k].nan_to_num(nan=7.0)), \
             f"{k}: differs with NaN margins around the inputs (an out-of-bounds read)"
         assert bool(torch.isfinite(ref[k]).all()), f"{k}: non-finite output on a healthy batch"
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+def test_guard_bands_hybrid_launch(per_date, dtype):
+    """The hybrid launch (two streams; 1,664 groups: 1,632 sequential + 32 twisted) under the same guards."""
+    d, T, B = 2, 203, 1664 * 32
+    run = _family_runs("hybrid", d, dtype, per_date, T, B)
+    ref, _ = run(False)
+    again, _ = run(False)
+    got, intact = run(True)
+    assert intact, "a kernel wrote outside its planes or its workspace"
+    for k in ref:
+        assert torch.equal(ref[k].nan_to_num(nan=7.0), again[k].nan_to_num(nan=7.0)), f"{k}: not deterministic"
+        assert torch.equal(ref[k].nan_to_num(nan=7.0), got[k].nan_to_num(nan=7.0)), k
