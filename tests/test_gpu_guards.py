@@ -66,8 +66,11 @@ def _family_runs(family, d, dtype, per_date, T, B, C=3):
         x = synth.make_inputs_bands("hetero", C, B=B, T=T, d=d, device="cuda", dtype=dtype,
                                     lam_mode="per_date" if per_date else "scalar")
     else:
+        # (the twisted kernel keeps a group only if each half has >= 2d observed days: the iid mask, so its
+        # down sweep -- and its stores -- run under the guards)
         x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=dtype,
-                              lam_mode="per_date" if per_date else "scalar")
+                              lam_mode="per_date" if per_date else "scalar",
+                              mask="bernoulli" if family in ("twisted", "hybrid") else None)
     x = {k: x[k].contiguous() for k in ("y", "w", "lam", "g")}
     if family == "soft":
         x["w"] = (x["w"] * 0.75).contiguous()
