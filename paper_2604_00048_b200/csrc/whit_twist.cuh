@@ -31,7 +31,10 @@ namespace whit {
 template <int D, typename IO, bool PD, bool BWD>
 struct TwLayout {
   static constexpr int K = Tile<IO, D, false>::K;  // chunk rows as the single-series kernels
-  static constexpr int ST = 2;
+#ifndef WHIT_TW_ST
+#define WHIT_TW_ST 2
+#endif
+  static constexpr int ST = sizeof(IO) == 4 ? WHIT_TW_ST : 2;  // (fp64 tiles: two stages fill the CTA budget)
   static constexpr int PAIRS = 2;  // warp pairs per CTA
   static constexpr int ROW = 32 * (int)sizeof(IO);
   static constexpr int OFF_RHS = 0;
