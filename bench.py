@@ -70,6 +70,9 @@ def parse(argv=None):
     ap.add_argument("--dist-smoke", action="store_true",
                     help="initialise the NCCL process group even at world size 1 (under torchrun) so the "
                          "barrier / all_reduce / all_gather paths of the multi-GPU run execute on one GPU")
+    ap.add_argument("--checksum-ranges", type=int, default=0,
+                    help="weak scaling, N = 1: also solve the global series ranges [r*B, (r+1)*B) for r < R (untimed) "
+                         "and report their output checksums -- rank r of an N = R run must reproduce range r bit for bit")
     ap.add_argument("--dist-check", action="store_true",
                     help="run only the multi-process plumbing (shards, rank-keyed inputs, barrier, max over "
                          "ranks, checksum gather; NCCL with GPUs, gloo without) on a small workload and print a "
@@ -640,6 +643,21 @@ def run_fwdbwd(args, P, synth, dev, stream, ws_n, rank):
     # rank r's checksum is the same at every world size (results are bitwise independent of placement).
     checksums = gather_checksums((z,) if fwd_only else (z, gy, gl), ws_n)
     checksums["tensors"] = "z" if fwd_only else "z, grad_y, grad_lambda"
+    if args.checksum_ranges > 1 and ws_n == 1 and not strong:
+        # the ranges ranks 1..R-1 of an N = R weak-scaling run own, solved here (untimed) for the bitwise check
+        ranges = [checksums["per_rank"][0]]
+        for r in range(1, args.checksum_ranges):
+            xr = synth.make_inputs(cfg, B=B, series_offset=r * B, device=dev, dtype=io)
+            wr = P.Workspace(d, T, B, io, per_date, device=dev, stream=stream)
+            zr, gyr, glr = torch.empty_like(xr["y"]), torch.empty_like(xr["y"]), torch.empty_like(xr["lam"])
+            P.whit_forward(xr["y"], xr["w"], xr["lam"], d, T, B, zr, wr)
+            if not fwd_only:
+                P.whit_backward(xr["g"], wr, zr, gyr, glr)
+            torch.cuda.synchronize(dev)
+            ranges.append(local_checksums((zr,) if fwd_only else (zr, gyr, glr)))
+            del xr, wr, zr, gyr, glr
+            torch.cuda.empty_cache()
+        checksums["ranges_at_n1"] = ranges
 
     nbin, nwarps = P.whit_wbits_detected(wsp)  # warps of the last forward that read W as bits
     wdet = nbin == nwarps and nwarps > 0
