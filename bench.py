@@ -299,7 +299,7 @@ def algorithmic_bytes(B: int, T: int, d: int, esz: int, per_date: bool, K: int |
     C = math.ceil(T / K)
     nfac, nrhs = d + d * (d - 1) // 2, d
     lam_rows = (T - d) if per_date else 0
-    lam_dn = (lam_rows + C * d) if per_date else 0          # down-sweep boxes carry d extra lambda rows
+    lam_dn = lam_rows  # (the d rows by which adjacent down-sweep boxes overlap come from L2, not HBM)
     bitrow = 4 * math.ceil(T / 32) / T                       # bytes of bit-packed w per date
     wrow = bitrow if wbits else esz
     w_fwd = T * (esz + bitrow + bitrow) if wdet else 2 * T * wrow  # wdet: float up, bits written + read
@@ -329,16 +329,17 @@ def variance_bytes(B: int, T: int, d: int, esz: int, per_date: bool):
     K = chunk_rows(d)
     C = math.ceil(T / K)
     nfac = d + d * (d - 1) // 2
-    lam = ((T - d) + (T - d + C * d)) if per_date else 0
+    lam = 2 * (T - d) if per_date else 0  # (box overlaps come from L2)
     return (2 * T * esz + lam * esz + T * esz + 2 * C * nfac * 8 + (0 if per_date else esz) + 4) * B
 
 
 def irregular_bytes(B: int, T: int, d: int, esz: int, per_date: bool, K: int = 8):
-    """Single-series uneven grid (K = 8 row chunks): the dates tile carries K + 2d rows per chunk."""
+    """Single-series uneven grid (K = 8 row chunks): inputs (and the dates) read in both sweeps, outputs once,
+    fp64 checkpoints; the dates tile carries K + 2d rows per chunk, the overlap served by L2."""
     C = math.ceil(T / K)
     nfac, nrhs = d + d * (d - 1) // 2, d
-    lam = ((T - d) + (T - d + C * d)) if per_date else 0
-    times = 2 * (T + 2 * d * C)
+    lam = 2 * (T - d) if per_date else 0
+    times = 2 * T  # (the 2d rows by which adjacent date boxes overlap come from L2)
     fwd = (2 * T * esz + 2 * T * esz + lam * esz + times * esz + (2 * T - d) * esz + 2 * C * (nfac + nrhs) * 8 + 4) * B
     bwd = (2 * T * esz + 2 * T * esz + lam * esz + times * esz + (T - d) * esz + T * esz
            + ((T - d) if per_date else 1) * esz + 2 * C * nrhs * 8 + C * nfac * 8 + 4) * B
@@ -350,8 +351,8 @@ def bands_bytes(B: int, T: int, d: int, C: int, esz: int, per_date: bool, K: int
     both sweeps once per pixel; each band reads its right-hand side twice and writes its outputs once."""
     Cc = math.ceil(T / K)
     nfac = d + d * (d - 1) // 2
-    lam = ((T - d) + (T - d + Cc * d)) if per_date else 0
-    times = 2 * (T + 2 * d * Cc) if irr else 0
+    lam = 2 * (T - d) if per_date else 0  # (box overlaps come from L2)
+    times = 2 * T if irr else 0
     shared = (2 * T + lam + times) * esz + Cc * nfac * 8 + 4
     fwd = (shared + Cc * nfac * 8 + C * (2 * T * esz + (2 * T - d) * esz + 2 * Cc * d * 8)) * B
     bwd = (shared + C * (2 * T * esz + (T - d) * esz + T * esz + 2 * Cc * d * 8)
@@ -369,12 +370,16 @@ def load_profile_summary():
         return None
 
 
-def profile_fields(kernel: str) -> dict | None:
+def profile_fields(kernel: str, workload: str | None = None) -> dict | None:
+    """The committed ncu figures of a launch: '<workload>/<launch>' entries (NEXT-row workloads), else the
+    headline's '<launch>' entries (hetero).  None if the profile has no entry for it."""
     prof = load_profile_summary() or {}
-    k = prof.get(kernel)
+    key = f"{workload}/{kernel}" if workload else kernel
+    k = prof.get(key)
     if not isinstance(k, dict):
         return None
-    out = {"traffic": k.get("dram_bytes_per_launch"), "traffic_source": prof.get("source")}
+    out = {"traffic": k.get("dram_bytes_per_launch"),
+           "traffic_source": prof.get("workloads_source" if workload else "source")}
     if "fp64_pipe_pct" in k:
         out["fp64_pipe_pct"] = k["fp64_pipe_pct"]
     return out
@@ -764,7 +769,8 @@ def run_op(args, P, synth, dev, stream, ws_n, rank):
             args, metric, ws_n * B / (ms / 1e3), UNIT, ws_n, ms, len(launches) * args.steps,
             {"workload": args.config, "op": args.op, "B_per_gpu": B, "T": T, "d": d, "lambda": cfg.lam_mode,
              "io": args.io, "l2": "inputs larger than L2"},
-            roofline=roofline(kb, per, ms), clocks=clocks)), flush=True)
+            roofline=roofline(kb, per, ms, traffic=profile_fields(max(per, key=per.get), args.op)), clocks=clocks)),
+            flush=True)
     return 0
 
 
@@ -791,7 +797,8 @@ def run_irregular(args, P, synth, dev, stream, ws_n, rank):
             ws_n * B / (ms / 1e3), UNIT, ws_n, ms, 2 * args.steps,
             {"workload": "irregular", "B_per_gpu": B, "T": T, "d": d, "io": args.io,
              "times": "cumulative gaps U{1..12} days", "l2": "inputs larger than L2"},
-            roofline=roofline({"whit_forward_times": fb, "whit_backward": bb}, per, ms), clocks=clocks,
+            roofline=roofline({"whit_forward_times": fb, "whit_backward": bb}, per, ms,
+                              traffic=profile_fields(max(per, key=per.get), "irregular")), clocks=clocks,
             paper_context="Table 1 (V100, PyTorch, T=350, C=10, order 2, batch 28672): 0.14 s "
                           "-> ~2.0 M band-series/s")), flush=True)
     return 0
@@ -822,7 +829,8 @@ def run_table1(args, P, synth, dev, stream, ws_n, rank):
             ws_n * B * C / (ms / 1e3), "band-series/s", ws_n, ms, 2 * args.steps,
             {"workload": "table1", "bands": C, "pixels_per_gpu": B, "T": T, "d": d, "io": args.io,
              "times": "cumulative gaps U{1..12} days", "l2": "inputs larger than L2"},
-            roofline=roofline({"whit_forward_times_bands": fb, "whit_backward_bands": bb}, per, ms), clocks=clocks,
+            roofline=roofline({"whit_forward_times_bands": fb, "whit_backward_bands": bb}, per, ms,
+                              traffic=profile_fields(max(per, key=per.get), "table1")), clocks=clocks,
             pixels_per_s=ws_n * B / (ms / 1e3),
             paper_context="Table 1 (V100, PyTorch banded, T=350, C=10, order 2, batch 28672): "
                           "0.14 s -> ~2.0 M band-series/s")), flush=True)
@@ -872,7 +880,8 @@ def run_s2tile(args, P, synth, dev, stream, ws_n, rank):
             torch.cuda.empty_cache()
     px_job = S2TILE_PIXELS if strong else ws_n * S2TILE_CHUNK
     fb, bb = bands_bytes(Bp_rank, T, d, C, esz, True)
-    roof = roofline({"whit_forward_bands": fb, "whit_backward_bands": bb}, per_sum, total_ms)
+    roof = roofline({"whit_forward_bands": fb, "whit_backward_bands": bb}, per_sum, total_ms,
+                    traffic=profile_fields(max(per_sum, key=per_sum.get), "s2tile") if not strong else None)
     # end to end from pinned HOST memory through whit_run_host_bands (pixel chunks streamed through the
     # shared-factor kernels, copies overlapped with compute), on the last resident chunk
     e2e = None
