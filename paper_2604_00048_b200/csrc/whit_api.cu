@@ -956,8 +956,9 @@ whit_status whit_posterior_variance(const void* w, const void* lambda, int d, in
   whit_status st = fill_params(ws, &p, w /* unused rhs slot */, w, lambda);
   if (st != WHIT_OK) return st;
   if ((st = wmap(ws, &p.tm_out0, var, ws->dt, B, T, ws->kk, 1)) != WHIT_OK) return st;
-  // the factor checkpoints are shared with the forward: a different (w, lambda) invalidates its backward
-  if (w != ws->w || lambda != ws->lam) ws->have_fwd = false;
+  // the factor checkpoints are shared with the forward: a different (w, lambda) invalidates its backward, and
+  // so does any forward whose checkpoints are not the sequential layout this kernel rewrites (twisted / hybrid)
+  if (w != ws->w || lambda != ws->lam || ws->tw) ws->have_fwd = false;
   ws->have_info = true;  // (set at enqueue: info is written by this launch)
   const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
   if (ws->dt == WHIT_F32)
