@@ -186,3 +186,20 @@ def test_hybrid_launch(per_date, dtype):
         z = a["z"][:, b].double().cpu().numpy()
         assert np.max(np.abs(z - o["z"].astype(float))) / ymax_observed(h["y"][b], h["w"][b]) <= tz, b
         assert rel_series(a["ybar"][:, b].double().cpu().numpy(), o["ybar"]).max() <= tg, b
+
+
+def test_posterior_variance_after_twisted_forward_invalidates_backward():
+    """whit_posterior_variance rewrites the factor checkpoints in the sequential layout, so after a twisted
+    forward the matching backward must be refused (WHIT_ERR_STATE), not run on the wrong layout."""
+    import paper_2604_00048_b200 as P
+    d, T, B = 2, 300, 64
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", mask="bernoulli")
+    ws = P.Workspace(d, T, B, torch.float32, True)
+    ws.set_twist(1)
+    z, gy, gl, var = (torch.empty_like(x["y"]), torch.empty_like(x["y"]), torch.empty_like(x["lam"]),
+                      torch.empty_like(x["y"]))
+    P.whit_forward(x["y"], x["w"], x["lam"], d, T, B, z, ws)
+    P.whit_posterior_variance(x["w"], x["lam"], d, T, B, var, ws)
+    with pytest.raises(P.WhitError) as e:
+        P.whit_backward(x["g"], ws, z, gy, gl)
+    assert e.value.status == 6  # WHIT_ERR_STATE
