@@ -545,7 +545,7 @@ def run_dist_check(args):
     import synth
     ws_n, rank, local = dist_env()
     cuda = torch.cuda.is_available()
-    if ws_n > 1 or args.dist_smoke:
+    if ws_n > 1 or (args.dist_smoke and "RANK" in os.environ):
         if cuda:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -591,7 +591,7 @@ def run_libwhit(args):
     ws_n, rank, local = dist_env()
     if ws_n != args.gpus and rank == 0:
         print(f"note: --gpus {args.gpus} but WORLD_SIZE={ws_n}; running {ws_n} rank(s)", file=sys.stderr)
-    if ws_n > 1 or args.dist_smoke:
+    if ws_n > 1 or (args.dist_smoke and "RANK" in os.environ):  # (--dist-smoke needs torchrun's env)
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local if ws_n > 1 else 0)
