@@ -18,7 +18,18 @@
 
 #include "whit_launch.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 using whit::Params;
+
+// NVTX range around each compute entry point (tracing: ncu --nvtx / nsys timelines); a no-op without a tool.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define WHIT_NVTX(name) NvtxRange whit_nvtx_range_(name)
 
 namespace {
 thread_local std::string g_err;
@@ -640,6 +651,7 @@ void whit_ws_destroy(whit_ws* ws) {
 
 whit_status whit_forward_bands(const void* y, const void* w, const void* lambda, int d, int64_t T, int64_t B, int C,
                                void* z, whit_ws* ws) {
+  WHIT_NVTX("whit_forward_bands");
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (ws->irr) return fail(WHIT_ERR_STATE, "irregular-grid workspace: use whit_forward_times");
   if (!y || !w || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
@@ -725,6 +737,7 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
 
 whit_status whit_forward_wbits(const void* y, const uint32_t* wbits, const void* lambda, int d, int64_t T, int64_t B,
                                void* z, whit_ws* ws) {
+  WHIT_NVTX("whit_forward_wbits");
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (ws->irr || ws->nb != 1) return fail(WHIT_ERR_STATE, "bit-packed W needs a single-band daily-grid workspace");
   if (!y || !wbits || !lambda || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
@@ -769,6 +782,7 @@ whit_status whit_pack_mask(const void* w, int64_t T, int64_t B, whit_dtype dtype
 
 whit_status whit_forward_times_bands(const void* y, const void* w, const void* lambda, const void* times, int d,
                                      int64_t T, int64_t B, int C, void* z, whit_ws* ws) {
+  WHIT_NVTX("whit_forward_times_bands");
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!ws->irr) return fail(WHIT_ERR_STATE, "workspace not created by whit_ws_create_times(_bands)");
   if (!y || !w || !lambda || !times || !z) return fail(WHIT_ERR_ARG, "NULL data pointer");
@@ -803,6 +817,7 @@ whit_status whit_forward_times(const void* y, const void* w, const void* lambda,
 
 whit_status whit_forward_mse(const void* y, const void* w, const void* lambda, const void* loss_w, int d, int64_t T,
                              int64_t B, void* z, void* grad_z, void* loss, whit_ws* ws) {
+  WHIT_NVTX("whit_forward_mse");
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!y || !w || !lambda || !loss_w || !z || !grad_z || !loss) return fail(WHIT_ERR_ARG, "NULL data pointer");
   if (ws->nb != 1 || ws->irr) return fail(WHIT_ERR_SHAPE, "the fused loss needs a single-band daily-grid workspace");
@@ -851,6 +866,7 @@ whit_status whit_forward(const void* y, const void* w, const void* lambda, int d
 }
 
 whit_status whit_backward(const void* grad_z, whit_ws* ws, const void* z, void* grad_y, void* grad_lambda) {
+  WHIT_NVTX("whit_backward");
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "whit_backward without a preceding whit_forward on this workspace");
   if (!grad_z || !grad_y || !grad_lambda) return fail(WHIT_ERR_ARG, "NULL data pointer");
@@ -915,6 +931,7 @@ whit_status whit_backward_bands(const void* grad_z, whit_ws* ws, const void* z, 
 }
 
 whit_status whit_grad_w(whit_ws* ws, const void* y, const void* z, const void* grad_y, void* grad_w) {
+  WHIT_NVTX("whit_grad_w");
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!ws->have_fwd) return fail(WHIT_ERR_STATE, "whit_grad_w without a preceding forward on this workspace");
   if (ws->wbits || !ws->w) return fail(WHIT_ERR_STATE, "whit_grad_w needs the float weight plane (not bit-packed W)");
@@ -941,6 +958,7 @@ whit_status whit_grad_w(whit_ws* ws, const void* y, const void* z, const void* g
 
 whit_status whit_posterior_variance(const void* w, const void* lambda, int d, int64_t T, int64_t B, void* var,
                                     whit_ws* ws) {
+  WHIT_NVTX("whit_posterior_variance");
   if (!ws) return fail(WHIT_ERR_ARG, "factor_ws is NULL");
   if (!w || !lambda || !var) return fail(WHIT_ERR_ARG, "NULL data pointer");
   if (ws->nb != 1 || ws->irr) return fail(WHIT_ERR_SHAPE, "posterior variance needs a single-band daily-grid workspace");
