@@ -551,11 +551,103 @@ struct Sweep {
     return 0;
   }
 
-  // ---- down sweep over one chunk: recompute the factor from the restored state,
-  // then back-substitute rows t0+K-1..t0 and emit outputs.
-  // Outputs of row t0+k go to the warp's staging tiles so0/so1 (row k, this
-  // lane's column); the caller writes them out with TMA stores, which clip
-  // rows past T (z, grad_y) or T-d (D z, grad_lambda) and columns past B.
+  // ---- one row of the down-sweep recompute: the factor row k (t = t0 + k) of a chunk from the running
+  // state, into (Arow, qk = v_t / D_t).  RAGGED: rows past T give q = 0, A = 0 (z = 0 exactly there).
+  template <bool RAGGED, bool UB>
+  static __device__ __forceinline__ void rec_row(FState<D>& st, const unsigned char* stg, int lane, int k, int t0,
+                                                 int T, double lam_s, uint32_t wm, bool ub_rt, double (&Arow)[D],
+                                                 double& qk) {
+    const bool ub = UB || ub_rt;
+    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
+    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
+    const int t = t0 + k;
+    IO wio;
+    double w;
+    row_w<IO>(t_w, wm, k, wio, w, ub);
+    double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
+    if (!PD && RAGGED) lt = (t < T - D) ? lt : 0.0;
+    const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
+    double Dt, idt, vt;
+    ldl_step<D, Newton<IO, D>::N>(st, w, lt, bb, Arow, Dt, idt, vt);
+    qk = vt * idt;
+    if (RAGGED && t >= T) {
+      qk = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) Arow[j] = 0.0;
+    }
+  }
+
+  // ---- one row of the back substitution: z_t = q_t - sum_j (M_j + A[t+j][j]) z[t+j] with win[i] = the A row of
+  // t+1+i, then the row's outputs: z and D z (forward; fused loss), or w u and -(D u)(D z) (backward).
+  // Outputs of row t0+k go to the warp's staging tiles so0/so1 (row k, this lane's column; the caller writes
+  // them out with TMA stores, which clip rows past T / T-d and columns past B) or, DIRECT, straight to HBM.
+  template <bool RAGGED, bool UB>
+  static __device__ __forceinline__ void back_row(int k, double qk, const double (&win)[D][D], double (&zw)[D],
+                                                  double& lam_acc, const unsigned char* stg, int lane, int t0, int T,
+                                                  IO* so0, IO* so1, double two_over_T, uint32_t wm, IO* gz0,
+                                                  long long Bst, bool valid, IO* gl0, bool ub_rt) {
+    const bool ub = UB || ub_rt;
+    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
+    const IO* t_dz = reinterpret_cast<const IO*>(stg + L::OFF_DZ) + lane;
+    const int TmD = T - D;
+    const int t = t0 + k;
+    double z = qk;
+#pragma unroll
+    for (int j = D; j >= 1; --j) {  // z[t+1] (just computed) enters last
+      z = fma(-Mj(D, j), zw[j - 1], z);
+      z = fma(-win[j - 1][j - 1], zw[j - 1], z);
+    }
+    // (D z)_t = sum_j c_j z[t+j]  (rows t <= T-d-1)
+    double dz = Cj(D, 0) * z;
+#pragma unroll
+    for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[j - 1], dz);
+#pragma unroll
+    for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
+    zw[0] = z;
+    if (!BWD) {
+      if (L::FDIRECT) {  // gz0: z rows, gl0: D z rows of this chunk
+        if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = from_f64<IO>(z);
+        if (valid && (!RAGGED || t < T - D)) gl0[(long long)k * Bst] = from_f64<IO>(dz);
+      } else {
+        so0[k * 32] = from_f64<IO>(z);
+        so1[k * 32] = from_f64<IO>(dz);
+      }
+      if (LOSS) {  // masked MSE: L += lw (z - y)^2 / T, g = 2 lw (z - y) / T
+        const IO lw = reinterpret_cast<const IO*>(stg + L::OFF_LW)[lane + k * 32];
+        const IO yr = reinterpret_cast<const IO*>(stg + L::OFF_RHS)[lane + k * 32];
+        const double e = (lw != IO(0)) ? z - to_f64<IO>(yr) : 0.0;  // unscored dates: exactly 0 (y may be NaN)
+        const double lwe = to_f64<IO>(lw) * e;
+        if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = from_f64<IO>(two_over_T * lwe);
+        if (!RAGGED || t < T) lam_acc = fma(lwe, e, lam_acc);  // (forward: lam_acc holds the loss sum)
+      }
+    } else {
+      IO gy, gl = IO(0);
+      IO wk;
+      double wkd;
+      row_w<IO>(t_w, wm, k, wk, wkd, ub);  // (bits: the exact 1 / 0 the float plane holds)
+      if (sizeof(IO) == 4 && PD) {
+        // fp32 I/O: w*u and -(Du)(Dz) formed from u, Du rounded once to fp32 (<= 1.5 ulp fp32)
+        gy = wk * from_f64<IO>(z);
+        gl = -(from_f64<IO>(dz) * t_dz[k * 32]);  // D z tile is 0 past row T-d-1
+      } else {
+        gy = from_f64<IO>(wkd * z);
+        const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
+        if (PD) gl = from_f64<IO>(g);
+        else if (!RAGGED || t < TmD) lam_acc += g;
+      }
+      if (L::BDIRECT) {  // gz0: grad_y rows, gl0: grad_lambda rows of this chunk
+        if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = gy;
+        if (PD && valid && (!RAGGED || t < TmD)) gl0[(long long)k * Bst] = gl;
+      } else {
+        so0[k * 32] = gy;
+        if (PD) so1[k * 32] = gl;
+      }
+    }
+  }
+
+  // ---- down sweep over one chunk: recompute the factor from the restored state, then back-substitute rows
+  // t0+K-1..t0 and emit outputs.  cA: the A rows t0+K.. of the chunk processed before (later in time).
   // UB: W read as bits in this chunk (compile-time: the forward picks the instantiation after its warp vote)
   template <bool RAGGED, bool UB = WB>
   static __device__ __forceinline__ void down_chunk(FState<D>& st, double (&cA)[D][D], double (&zw)[D],
@@ -564,96 +656,26 @@ struct Sweep {
                                                     double two_over_T = 0.0, uint32_t wm = 0, IO* gz0 = nullptr,
                                                     long long Bst = 0, bool valid = false, IO* gl0 = nullptr,
                                                     bool ub_rt = WB) {
-    // UB = true: bits at compile time; otherwise the runtime flag (the plain forward before / without
-    // the compile-time instantiation)
-    const bool ub = UB || ub_rt;
-    const IO* t_rhs = reinterpret_cast<const IO*>(stg + L::OFF_RHS) + lane;
-    const IO* t_w = reinterpret_cast<const IO*>(stg + L::OFF_W) + lane;
-    const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
-    const IO* t_dz = reinterpret_cast<const IO*>(stg + L::OFF_DZ) + lane;
-    const int TmD = T - D;
     double q[K];
     double Ak[K][D];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int t = t0 + k;
-      IO wio;
-      double w;
-      row_w<IO>(t_w, wm, k, wio, w, ub);
-      double lt = PD ? to_f64<IO>(t_lam[(k + D) * 32]) : lam_s;
-      if (!PD && RAGGED) lt = (t < TmD) ? lt : 0.0;
-      const double bb = rhs_times_w<IO, BWD>(t_rhs[k * 32], wio, w);
-      double Dt, idt, vt;
-      ldl_step<D, Newton<IO, D>::N>(st, w, lt, bb, Ak[k], Dt, idt, vt);
-      q[k] = vt * idt;
-      if (RAGGED && t >= T) {  // rows past the end: z = 0 exactly (q = 0, A = 0, zero window)
-        q[k] = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) Ak[k][j] = 0.0;
-      }
-    }
+    for (int k = 0; k < K; ++k) rec_row<RAGGED, UB>(st, stg, lane, k, t0, T, lam_s, wm, ub_rt, Ak[k], q[k]);
 #pragma unroll
     for (int k = K - 1; k >= 0; --k) {
-      const int t = t0 + k;
-      double z = q[k];
+      double win[D][D];
 #pragma unroll
-      for (int j = D; j >= 1; --j) {  // z[t+1] (just computed) enters last
-        const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
-        z = fma(-Mj(D, j), zw[j - 1], z);
-        z = fma(-a, zw[j - 1], z);
-      }
-      // (D z)_t = sum_j c_j z[t+j]  (rows t <= T-d-1)
-      double dz = Cj(D, 0) * z;
+      for (int i = 0; i < D; ++i)
 #pragma unroll
-      for (int j = 1; j <= D; ++j) dz = fma(Cj(D, j), zw[j - 1], dz);
-#pragma unroll
-      for (int i = D - 1; i >= 1; --i) zw[i] = zw[i - 1];
-      zw[0] = z;
-      if (!BWD) {
-        if (L::FDIRECT) {  // gz0: z rows, gl0: D z rows of this chunk
-          if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = from_f64<IO>(z);
-          if (valid && (!RAGGED || t < T - D)) gl0[(long long)k * Bst] = from_f64<IO>(dz);
-        } else {
-          so0[k * 32] = from_f64<IO>(z);
-          so1[k * 32] = from_f64<IO>(dz);
-        }
-        if (LOSS) {  // masked MSE: L += lw (z - y)^2 / T, g = 2 lw (z - y) / T
-          const IO lw = reinterpret_cast<const IO*>(stg + L::OFF_LW)[lane + k * 32];
-          const IO yr = reinterpret_cast<const IO*>(stg + L::OFF_RHS)[lane + k * 32];
-          const double e = (lw != IO(0)) ? z - to_f64<IO>(yr) : 0.0;  // unscored dates: exactly 0 (y may be NaN)
-          const double lwe = to_f64<IO>(lw) * e;
-          if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = from_f64<IO>(two_over_T * lwe);
-          if (!RAGGED || t < T) lam_acc = fma(lwe, e, lam_acc);  // (forward: lam_acc holds the loss sum)
-        }
-      } else {
-        IO gy, gl = IO(0);
-        IO wk;
-        double wkd;
-        row_w<IO>(t_w, wm, k, wk, wkd, ub);  // (bits: the exact 1 / 0 the float plane holds)
-        if (sizeof(IO) == 4 && PD) {
-          // fp32 I/O: w*u and -(Du)(Dz) formed from u, Du rounded once to fp32 (<= 1.5 ulp fp32)
-          gy = wk * from_f64<IO>(z);
-          gl = -(from_f64<IO>(dz) * t_dz[k * 32]);  // D z tile is 0 past row T-d-1
-        } else {
-          gy = from_f64<IO>(wkd * z);
-          const double g = -dz * to_f64<IO>(t_dz[k * 32]);  // D z tile is 0 past row T-d-1
-          if (PD) gl = from_f64<IO>(g);
-          else if (!RAGGED || t < TmD) lam_acc += g;
-        }
-        if (L::BDIRECT) {  // gz0: grad_y rows, gl0: grad_lambda rows of this chunk
-          if (valid && (!RAGGED || t < T)) gz0[(long long)k * Bst] = gy;
-          if (PD && valid && (!RAGGED || t < TmD)) gl0[(long long)k * Bst] = gl;
-        } else {
-          so0[k * 32] = gy;
-          if (PD) so1[k * 32] = gl;
-        }
-      }
+        for (int j = 0; j < D; ++j) win[i][j] = (k + 1 + i < K) ? Ak[k + 1 + i][j] : cA[k + 1 + i - K][j];
+      back_row<RAGGED, UB>(k, q[k], win, zw, lam_acc, stg, lane, t0, T, so0, so1, two_over_T, wm, gz0, Bst, valid,
+                           gl0, ub_rt);
     }
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) cA[i][j] = Ak[i][j];
   }
+
 };
 
 // ------------------------------------------------------------------ the kernel
