@@ -299,7 +299,9 @@ whit_status whit_failures(whit_ws* ws, int64_t* n_failed, int32_t* host_info);
 const int32_t* whit_info_device(const whit_ws* ws);
 
 /* Execution path of whit_forward / whit_backward on a single-band daily-grid
- * workspace.  Small batches take the TWISTED path (two warps per group of 32
+ * workspace: the same solve of Eq. (3) and the same backward
+ * by a different elimination order of the banded SPD system (
+ * DESIGN.md R-21) -- results agree to rounding.  Small batches take the TWISTED path (two warps per group of 32
  * series: one factors the first half of the dates forward, the other the
  * second half in reversed time; they meet in a d x d block -- half the
  * per-series latency, twice the warps in flight); a group whose halves are
@@ -320,7 +322,8 @@ whit_status whit_ws_set_twist(whit_ws* ws, int mode);
 whit_status whit_twist_groups(whit_ws* ws, int64_t* n_twisted, int64_t* n_groups);
 
 /* SYNCHRONISES the workspace stream, then reports how many of the last plain
- * whit_forward's warps (groups of 32 consecutive series) found a binary W and
+ * whit_forward's warps (groups of 32 consecutive series) found a binary W (the
+ * paper's W is 0/1) and
  * read it as bits (*n_binary) out of *n_warps = ceil(B/32).  *n_binary = 0 if
  * the last forward was not the plain float-W forward or the detection is off.
  * Diagnostic (tests, bench); WHIT_ERR_STATE if no forward ran. */
