@@ -106,6 +106,22 @@ def test_call_validation_before_launch(L):
     L.whit_ws_destroy(None)
 
 
+def test_path_and_diagnostic_entry_points_validate(L):
+    """whit_ws_set_twist / whit_twist_groups / whit_wbits_detected: argument and state checks on the host."""
+    h = ctypes.c_void_p()
+    assert L.whit_ws_create(ctypes.byref(h), 2, 100, 128, 0, 1, ctypes.c_void_p(1 << 20), 1 << 40, None) == 0
+    for mode in (-1, 0, 1, 2):
+        assert L.whit_ws_set_twist(h, mode) == 0
+    assert L.whit_ws_set_twist(h, 3) == 1 and L.whit_ws_set_twist(h, -2) == 1
+    assert L.whit_ws_set_twist(None, 0) == 1
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    assert L.whit_twist_groups(h, ctypes.byref(a), ctypes.byref(b)) == 6      # no forward yet
+    assert L.whit_wbits_detected(h, ctypes.byref(a), ctypes.byref(b)) == 6
+    assert L.whit_twist_groups(h, None, ctypes.byref(b)) == 1
+    assert L.whit_wbits_detected(None, ctypes.byref(a), ctypes.byref(b)) == 1
+    L.whit_ws_destroy(h)
+
+
 def test_python_binding_refuses_cpu_tensors():
     import paper_2604_00048_b200 as P
     y = torch.zeros(10, 4)
