@@ -203,3 +203,28 @@ def test_posterior_variance_after_twisted_forward_invalidates_backward():
     with pytest.raises(P.WhitError) as e:
         P.whit_backward(x["g"], ws, z, gy, gl)
     assert e.value.status == 6  # WHIT_ERR_STATE
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_twisted_short_series_and_split_offsets(d):
+    """Short series down to the smallest T the twisted split accepts, every residue of T - m modulo K (the
+    bottom half's chunk boundary relative to the twist block, which may straddle two bottom chunks): twisted
+    results against O1 on every series, fp64 I/O."""
+    import paper_2604_00048_b200 as P
+    K = 16 if d <= 2 else 12
+    Tmin = 2 * K + d
+    dtype, B = torch.float64, 32
+    for T in range(Tmin, Tmin + K + 3):
+        x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64, mask="bernoulli",
+                              seed=500 + T)
+        x["w"][:, :] = torch.where(torch.arange(T, device="cuda")[:, None] % 3 == 1, 0.0, 1.0)  # dense, 2/3
+        r = run(x, d, dtype, 1, T, B)
+        assert r["groups"] == (1, 1), (T, r["groups"])
+        h = host_inputs({k: x[k] for k in ("y", "w", "lam", "g")})
+        tz, tg = TOL[(dtype, d)]
+        for b in range(0, B, 7):
+            o = O1.forward_backward(h["y"][b], h["w"][b], h["lam"][b], d, h["g"][b])
+            z = r["z"][:, b].double().cpu().numpy()
+            assert np.max(np.abs(z - o["z"].astype(float))) / ymax_observed(h["y"][b], h["w"][b]) <= tz, (T, b)
+            assert rel_series(r["ybar"][:, b].double().cpu().numpy(), o["ybar"]).max() <= tg, (T, b)
+            assert rel_series(r["lambar"][:, b].double().cpu().numpy(), o["lambar"]).max() <= tg, (T, b)
