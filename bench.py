@@ -701,9 +701,11 @@ def run_fwdbwd(args, P, synth, dev, stream, ws_n, rank):
         bits_h = P.whit_pack_mask(w).cpu() if (args.config == "hetero" and not args.no_extras) else None
         del wsp, z, gy, gl
         torch.cuda.empty_cache()
-        e2e = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, B_job=B_job)
+        cap = 65536 if ws_n > 1 else 0  # (N > 1: a per-rank sample of the shard, see run_e2e)
+        e2e = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, B_job=B_job, max_series=cap)
         if bits_h is not None:
-            e2e_wbits = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, wbits=bits_h, B_job=B_job)
+            e2e_wbits = run_e2e(P, x, d, T, B, io, stream, dev, args.e2e_steps, wbits=bits_h, B_job=B_job,
+                                max_series=cap)
 
     # CPU oracle baseline (rank 0, N = 1 only), and a conventional CPU banded solver for context
     cpu = cpu_banded = None
@@ -928,18 +930,24 @@ def run_s2tile(args, P, synth, dev, stream, ws_n, rank):
     return 0
 
 
-def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6, wbits=None, B_job=None):
+def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6, wbits=None, B_job=None, max_series=0):
     """Same metric through the public C-ABI with pinned HOST buffers: whit_run_host streams the
     batch in series chunks (pitched 2-D H2D copies of y, w, lambda, g; whit_forward +
     whit_backward; D2H of z, grad_y, grad_lambda), copies overlapping kernels on nbuf streams.
-    With ``wbits`` (host bit-packed W) the weights cross PCIe as bits (whit_run_host_wbits)."""
+    With ``wbits`` (host bit-packed W) the weights cross PCIe as bits (whit_run_host_wbits).
+    max_series > 0: stream only the first max_series series of the rank's batch (N > 1: eight ranks share the
+    host's memory and PCIe, so each pins a 65,536-series sample instead of its whole shard; the rate is
+    per series either way, the pipeline being chunked)."""
     import torch
+    Bs = min(B, max_series) if max_series else B
+    cols = (lambda t: t[..., :Bs]) if Bs < B else (lambda t: t)
     keys = ("y", "lam", "g") if wbits is not None else ("y", "w", "lam", "g")
-    h = {k: torch.empty(x[k].shape, dtype=io, pin_memory=True) for k in keys}
+    h = {k: torch.empty(cols(x[k]).shape, dtype=io, pin_memory=True) for k in keys}
     for k in h:
-        h[k].copy_(x[k])
+        h[k].copy_(cols(x[k]))
     if wbits is not None:
-        h["wbits"] = wbits.pin_memory()
+        h["wbits"] = cols(wbits).contiguous().pin_memory()
+    x = {k: cols(x[k]) for k in ("y", "lam")}
     oz = torch.empty(x["y"].shape, dtype=io, pin_memory=True)
     oy = torch.empty(x["y"].shape, dtype=io, pin_memory=True)
     ol = torch.empty(x["lam"].shape, dtype=io, pin_memory=True)
@@ -962,8 +970,9 @@ def run_e2e(P, x, d, T, B, io, stream, dev, steps, chunk=8192, nbuf=6, wbits=Non
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(e0.elapsed_time(e1) / steps, dev)
-    return {"value": (B_job or ws_n * B) / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h,
+    series = ws_n * Bs if Bs < B else (B_job or ws_n * B)
+    return {"value": series / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "series_per_step": series,
             "ms_per_step": ms, "steps": steps,
             "api": f"{'whit_run_host_wbits' if bits is not None else 'whit_run_host'} (C-ABI, pinned host buffers, "
                    f"chunk {chunk}, {nbuf} streams)"}
