@@ -228,3 +228,41 @@ def test_twisted_short_series_and_split_offsets(d):
             assert np.max(np.abs(z - o["z"].astype(float))) / ymax_observed(h["y"][b], h["w"][b]) <= tz, (T, b)
             assert rel_series(r["ybar"][:, b].double().cpu().numpy(), o["ybar"]).max() <= tg, (T, b)
             assert rel_series(r["lambar"][:, b].double().cpu().numpy(), o["lambar"]).max() <= tg, (T, b)
+
+
+def test_autograd_default_path_is_twisted_and_correct():
+    """The package default (no WHIT_TWIST in the environment): smooth() on a small batch takes the twisted path
+    (a subprocess, since the suite pins WHIT_TWIST=0) and its z and gradients match O1."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import json, torch, numpy as np, synth, paper_2604_00048_b200 as P
+from oracle import whittaker as O1
+d, T, B = 2, 400, 96
+x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64, mask="bernoulli", seed=3)
+y = x["y"].clone().requires_grad_(True); lam = x["lam"].clone().requires_grad_(True)
+z = P.smooth(y, x["w"], lam, d)
+(z * x["g"]).sum().backward()
+out = {"tw": None}
+ws = P.Workspace(d, T, B, torch.float64, True); zz = torch.empty_like(y)
+P.whit_forward(x["y"], x["w"], x["lam"], d, T, B, zz, ws); out["tw"] = P.whit_twist_groups(ws)
+errs = []
+for b in (0, 50, 95):
+    o = O1.forward_backward(*(t[:, b].cpu().numpy() for t in (x["y"], x["w"], x["lam"])), d, x["g"][:, b].cpu().numpy())
+    ym = np.abs(x["y"][:, b].cpu().numpy()[x["w"][:, b].cpu().numpy() > 0]).max()
+    errs.append([float(np.abs(z[:, b].detach().cpu().numpy() - o["z"].astype(float)).max() / ym),
+                 float(np.abs(y.grad[:, b].cpu().numpy() - o["ybar"].astype(float)).max() / np.abs(o["ybar"].astype(float)).max()),
+                 float(np.abs(lam.grad[:, b].cpu().numpy() - o["lambar"].astype(float)).max() / np.abs(o["lambar"].astype(float)).max())])
+out["errs"] = errs
+print(json.dumps(out))
+"""
+    env = {k: v for k, v in os.environ.items() if k not in ("WHIT_TWIST", "WHIT_HYBRID")}
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["tw"] == [3, 3], out
+    for ez, ey, el in out["errs"]:
+        assert ez <= 1e-10 and ey <= 1e-9 and el <= 1e-9, out["errs"]
