@@ -444,7 +444,12 @@ int hyb_pick(const whit_ws* ws) {
   const int m = tw_split(ws);
   if (m < ws->kk || ws->T - m - ws->d < ws->kk) return 0;
   const long long G = (ws->B + 31) / 32;
-  return (G > 148 * 12 && G <= hmax) ? kHybG1 : 0;
+  static const int g1 = [] {  // WHIT_HYB_G1: the sequential part's group count (dev A/B; even)
+    const char* v = std::getenv("WHIT_HYB_G1");
+    const int x = v ? std::atoi(v) : 0;
+    return (x >= 2 && x % 2 == 0) ? x : kHybG1;
+  }();
+  return (G > 148 * 12 && G <= hmax && G > g1) ? g1 : 0;
 }
 
 whit_status hyb_streams(whit_ws* ws) {
