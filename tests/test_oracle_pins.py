@@ -585,6 +585,34 @@ def test_mse_chain_rule_fd():
     assert abs(float(loss) - np.sum(lw * (z.astype(float) - y) ** 2) / T) < 1e-15
 
 
+def test_mse_loss_value_exact_on_polynomial_data():
+    """The loss VALUE pinned by the polynomial pass-through, not by restating its formula: observed data on a
+    line (degree < d) makes z that line exactly (pinned above); held-out dates carry dyadic offsets e_t, so
+    L = T^-1 sum lw_t e_t^2 and g = -2 T^-1 lw e are exact rationals the oracle must reproduce."""
+    from fractions import Fraction as F
+    T, d = 48, 2
+    t = np.arange(T, dtype=float)
+    line = 0.5 + 0.25 * t
+    w = np.ones(T)
+    held = np.array([4, 9, 17, 30, 41])
+    e = np.array([0.5, -1.25, 2.0, -0.375, 0.75])
+    w[held] = 0.0
+    y = line.copy()
+    y[held] += e
+    lw = np.zeros(T)
+    lw[held] = [1.0, 0.5, 1.0, 2.0, 1.0]
+    z, _ = O1.forward(y, w, 1e3, d)
+    assert np.max(np.abs(z.astype(float) - line)) < 1e-12
+    loss, g = O1.mse_loss_grad(line, y, lw)  # the exact z
+    exact = sum(F(float(lw[i])) * F(float(v)) ** 2 for i, v in zip(held, e)) / T
+    assert float(loss) == float(exact)
+    ge = np.zeros(T)
+    ge[held] = [-2 * float(lw[i]) * float(v) / T for i, v in zip(held, e)]
+    assert np.array_equal(g.astype(float), ge)
+    loss_o, _ = O1.mse_loss_grad(z, y, lw)  # through the solve: the same within rounding
+    assert abs(float(loss_o) - float(exact)) <= 1e-12 * float(exact)
+
+
 # ----------------------------------------------------------------- irregular grid (NEXT-2)
 def _uneven_times(T, lo=1, hi=12):
     return np.cumsum(rng.integers(lo, hi, size=T)).astype(float)
