@@ -327,7 +327,7 @@ template <int D> struct Ck {
 // ------------------------------------------------------------------ tiling config
 // One warp = 32 series = one TMA pipeline.  K time steps per chunk/tile, ST
 // ring stages per warp, WARPS warps per CTA.  K = 16 for d <= 2; d = 3 keeps
-// 4 fp64 values per chunk row in registers, so its chunk is 8 steps.
+// 4 fp64 values per chunk row in registers, so its chunk is 12 steps (WHIT_TILE_K3).
 // Registers are granted per SMSP file (16K regs each; cudaFuncGetAttributes:
 // maxThreadsPerBlock = 256 at 192 regs, 384 at 168), so 12 warps/SM need <= 168
 // regs.  Forward: 4-warp CTAs, 3 per SM (16.8 KB smem per warp).  Backward (one
