@@ -49,6 +49,12 @@ class WhittakerFn(torch.autograd.Function):
             raise TypeError("y, w, lambda must share a dtype")
         if times is not None and (times.shape != (T, B) or times.dtype != y.dtype):
             raise ValueError("times must be (T, B) of y's dtype")
+        if T < d + 1:
+            raise ValueError(f"T = {T} < d + 1 = {d + 1}: Omega needs at least d + 1 dates (P:87)")
+        ctx.empty = B == 0
+        if ctx.empty:  # an empty batch: nothing to solve (the C-ABI requires B >= 1)
+            ctx.shapes = (w.shape, lam.shape)
+            return torch.empty_like(y)
         q = 4 if y.dtype == torch.float32 else 2
         Bp = (B + q - 1) // q * q  # 16-byte row stride; padded series: w = 1, lam = 1, y = 0
         yp = _pad_cols(y, Bp, 0.0)
@@ -83,6 +89,10 @@ class WhittakerFn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, gz):
+        if ctx.empty:
+            new = lambda shape: gz.new_empty(shape)  # noqa: E731
+            gw = new(ctx.shapes[0]) if ctx.needs_input_grad[1] else None
+            return new(gz.shape), gw, new(ctx.shapes[1]), None, None
         ws = ctx.ws
         saved = ctx.saved_tensors
         wp, lp, z = saved[0], saved[1], saved[2]

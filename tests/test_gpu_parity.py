@@ -1072,3 +1072,23 @@ def test_scalar_lambda_mse_cotangent(d, dtype):
     _, _, n_well = check_scalar_lambar(gl.double().cpu().numpy(), lambar_r.astype(np.float64),
                                        np.sum(np.abs(terms.astype(np.float64)), axis=1), tg, f"mse d={d}")
     assert n_well >= 0.9 * B  # the realistic cotangent's gradient is well conditioned on most series
+
+
+@pytest.mark.parametrize("bands", [False, True])
+def test_empty_batch_through_autograd(bands):
+    """B = 0 (an empty tile): the shim returns empty z and gradients without a launch (the C-ABI itself
+    rejects B = 0 with WHIT_ERR_SHAPE, libwhit.h 'Sizes'); T < d + 1 is refused before any launch."""
+    import paper_2604_00048_b200 as P
+
+    T, d = 40, 2
+    shape = (3, T, 0) if bands else (T, 0)
+    y = torch.zeros(shape, device="cuda", requires_grad=True)
+    w = torch.ones(T, 0, device="cuda", requires_grad=True)
+    lam = torch.ones(T - d, 0, device="cuda", requires_grad=True)
+    z = P.smooth(y, w, lam, d)
+    assert z.shape == y.shape
+    z.sum().backward()
+    assert y.grad.shape == y.shape and lam.grad.shape == lam.shape and w.grad.shape == w.shape
+    with pytest.raises(Exception):
+        P.smooth(torch.zeros(2, 4, device="cuda"), torch.ones(2, 4, device="cuda"),
+                 torch.ones(4, device="cuda"), 2)
