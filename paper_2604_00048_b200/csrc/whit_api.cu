@@ -703,14 +703,15 @@ whit_status whit_forward_bands(const void* y, const void* w, const void* lambda,
     if (e == cudaSuccess)
       e = cudaMemsetAsync(ws->buf + ws->L.off_wflag + size_t(g1) * 4, 0, size_t(G - g1) * 4, ws->aux);
     if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid fork: %s", cudaGetErrorString(e));
-    if ((st = dispatch<false>(ws, ps)) != WHIT_OK) return st;
+    st = dispatch<false>(ws, ps);
     ws->stream = ws->aux;
-    st = dispatch_tw<false>(ws, pt);
+    if (st == WHIT_OK) st = dispatch_tw<false>(ws, pt);
     if (st == WHIT_OK) st = dispatch<false>(ws, p);
     ws->stream = main;
-    if (st != WHIT_OK) return st;
+    // join even when a launch on the auxiliary stream failed: nothing it enqueued may outlive the call unordered
     e = cudaEventRecord(ws->ev_join, ws->aux);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(main, ws->ev_join, 0);
+    if (st != WHIT_OK) return st;
     if (e != cudaSuccess) return fail(WHIT_ERR_CUDA, "hybrid join: %s", cudaGetErrorString(e));
     mark_forward(ws, w, lambda, z, nullptr, nullptr, wdet, true, g1);
     return WHIT_OK;
