@@ -318,6 +318,14 @@ __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, d
   for (int k = 0; k < D; ++k) s.ap[0][k] = A[k];
 }
 
+// 4-B global load under a predicate, into a register that keeps its value (0 here) when the predicate is off.
+__device__ __forceinline__ uint32_t ld_pred_u32(const uint32_t* a, bool ok) {
+  uint32_t v = 0u;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.u32 %0, [%1];\n\t}"
+               : "+r"(v) : "l"(a), "r"((uint32_t)ok) : "memory");
+  return v;
+}
+
 // Checkpoint field counts: factor part = D (Delta) + D(D-1)/2 (A), rhs part = D (v).
 template <int D> struct Ck {
   static constexpr int NFAC = D + D * (D - 1) / 2;
@@ -722,17 +730,28 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
   int nobs = 0, bad = 0;
   bool allpos = true;
   int it = 0;
-  // bits of W (WB, or WD once detected): the chunk's mask bits, prefetched one chunk ahead (plain coalesced
-  // 4-B loads)
-  auto wword = [&](int cc) -> uint32_t {
-    if (!ub || !valid || cc < 0 || cc >= C) return 0u;
-    // bits cc*K .. cc*K+K-1 of the series' mask; a chunk may straddle two words when K does not divide 32
+  // bits of W (WB, or WD once detected): the chunk's mask bits.  wload() issues the plain coalesced 4-B
+  // load(s) of the word(s) holding chunk cc's bits one chunk ahead; wbits_of() extracts them when the chunk
+  // starts -- only then, so the in-order warp does not wait on the load right after issuing it (it did:
+  // the shift next to the load was the backward's top stall in ncu's source view)
+  // (each word comes from a predicated load straight into the register that carries it to the next chunk:
+  // a plain `ok ? load : 0` compiled to a move right after the load, which waited on it.  K = 12 (d = 3): a
+  // chunk may straddle two words)
+  struct WRaw { uint32_t lo, hi; };
+  auto wload = [&](int cc) -> WRaw {
+    const bool ok = ub && valid && cc >= 0 && cc < C;
     const int bit0 = cc * K, r = bit0 >> 5, sh = bit0 & 31;
-    uint64_t two = p.wbits[(long long)r * B + b];
-    if (sh + K > 32 && (r + 1) * 32 < T) two |= (uint64_t)p.wbits[(long long)(r + 1) * B + b] << 32;
-    return (uint32_t)(two >> sh) & (K >= 32 ? 0xffffffffu : ((1u << K) - 1u));
+    const uint32_t* a = p.wbits + (long long)r * B + b;
+    WRaw v;
+    v.lo = ld_pred_u32(a, ok);
+    v.hi = (32 % K == 0) ? 0u : ld_pred_u32(a + B, ok && sh + K > 32 && (r + 1) * 32 < T);
+    return v;
   };
-  uint32_t wm_next = wword(0);
+  auto wbits_of = [&](WRaw v, int cc) -> uint32_t {
+    const uint64_t two = (uint64_t)v.lo | ((uint64_t)v.hi << 32);
+    return (uint32_t)(two >> ((cc * K) & 31)) & (K >= 32 ? 0xffffffffu : ((1u << K) - 1u));
+  };
+  WRaw wm_next = wload(0);
   uint64_t wacc = 0;   // WD: mask bits of rows wbase*32.. not yet stored
   int wbase = 0;
   bool isbin = true;   // WD: every w of this series so far is exactly 0 or 1
@@ -740,8 +759,8 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
   // ================================================================ up sweep
   for (int c = 0; c < C; ++c, ++it) {
     const int s = it % ST;
-    const uint32_t wm = wm_next;
-    wm_next = wword(c + 1);
+    const uint32_t wm = wbits_of(wm_next, c);
+    wm_next = wload(c + 1);
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const unsigned char* stg = ring + s * L::STAGE;
     const int t0 = c * K;
@@ -786,7 +805,7 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
     if (valid && wbase * 32 < T) p.wbits_out[(long long)wbase * B + b] = uint32_t(wacc);
     const bool all_bin = __all_sync(0xffffffffu, isbin || !valid);
     if (lane == 0) p.wflag[bw >> 5] = all_bin ? 1 : 0;
-    ub = all_bin;  // (this lane's own stores above are what wword() reads back)
+    ub = all_bin;  // (this lane's own stores above are what wload() reads back)
   }
 
   // Status (LAPACK xPBTRF style): fewer than d observed days -> T-d+1 (exactly
@@ -827,12 +846,12 @@ __device__ __forceinline__ void whit_body(const Params& p, unsigned char* ring, 
     }                                                                                             \
   } while (0)
   WHIT_LOAD_CK(C - 1);
-  wm_next = wword(C - 1);
+  wm_next = wload(C - 1);
 
   for (int c = C - 1; c >= 0; --c, ++it) {
     const int s = it % ST;
-    const uint32_t wm = wm_next;
-    wm_next = wword(c - 1);
+    const uint32_t wm = wbits_of(wm_next, c);
+    wm_next = wload(c - 1);
     mbar_wait(&bars[s], (uint32_t)((it / ST) & 1));
     const unsigned char* stg = ring + s * L::STAGE;
     const IO* t_lam = reinterpret_cast<const IO*>(stg + L::OFF_LAM) + lane;  // row k <-> t0 - D + k
