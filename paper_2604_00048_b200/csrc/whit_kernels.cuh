@@ -326,6 +326,16 @@ __device__ __forceinline__ uint32_t ld_pred_u32(const uint32_t* a, bool ok) {
   return v;
 }
 
+// 8-B global load under a predicate, likewise (checkpoints loaded a chunk ahead: `valid ? load : 0.0`
+// compiled to a move of the loaded value into the loop-carried register right after the load, i.e. a wait
+// on DRAM latency per chunk).
+__device__ __forceinline__ double ld_pred_f64(const double* a, bool ok) {
+  double v = 0.0;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.f64 %0, [%1];\n\t}"
+               : "+d"(v) : "l"(a), "r"((uint32_t)ok) : "memory");
+  return v;
+}
+
 // Checkpoint field counts: factor part = D (Delta) + D(D-1)/2 (A), rhs part = D (v).
 template <int D> struct Ck {
   static constexpr int NFAC = D + D * (D - 1) / 2;
@@ -1226,9 +1236,9 @@ __global__ void __maxnreg__((D == 3 ? 224 : 168)) whit_irr_kernel(const __grid_c
     const double* ckf = p.ck_fac + (long long)cc * NFAC * B + b;
     const double* ckr = ck_rhs + (long long)cc * D * B;
 #pragma unroll
-    for (int f = 0; f < NFAC; ++f) pck[f] = valid ? ckf[(long long)f * B] : 0.0;
+    for (int f = 0; f < NFAC; ++f) pck[f] = ld_pred_f64(ckf + (long long)f * B, valid);
 #pragma unroll
-    for (int i = 0; i < D; ++i) pv[i] = valid ? ckr[(long long)i * B] : 0.0;
+    for (int i = 0; i < D; ++i) pv[i] = ld_pred_f64(ckr + (long long)i * B, valid);
   };
   load_ck(C - 1);
   for (int c = C - 1; c >= 0; --c, ++it) {
@@ -1469,7 +1479,7 @@ __global__ void __maxnreg__(168) whit_var_kernel(const __grid_constant__ Params 
   auto load_ck = [&](int cc) {
     const double* ckf = p.ck_fac + (long long)cc * NFAC * B + b;
 #pragma unroll
-    for (int f = 0; f < NFAC; ++f) pck[f] = valid ? ckf[(long long)f * B] : 0.0;
+    for (int f = 0; f < NFAC; ++f) pck[f] = ld_pred_f64(ckf + (long long)f * B, valid);
   };
   load_ck(C - 1);
   for (int c = C - 1; c >= 0; --c, ++it) {

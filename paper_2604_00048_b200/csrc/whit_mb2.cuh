@@ -245,7 +245,7 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
     auto load_ck = [&](int c) {
       const double* ckf = p.ck_fac + (long long)c * NFAC * B + b;
 #pragma unroll
-      for (int f = 0; f < NFAC; ++f) ckn[f] = valid ? ckf[(long long)f * B] : 0.0;
+      for (int f = 0; f < NFAC; ++f) ckn[f] = ld_pred_f64(ckf + (long long)f * B, valid);
     };
     load_ck(C - 1);
     for (int c = C - 1; c >= 0; --c, ++it, ++fb) {
@@ -424,7 +424,7 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
       const double* ck = ck_rhs + (long long)c * ck_stride + (long long)(cb0 + u) * D * B;
       const bool ok = valid && u < nbw;
 #pragma unroll
-      for (int i = 0; i < D; ++i) vn[u][i] = ok ? ck[(long long)i * B] : 0.0;
+      for (int i = 0; i < D; ++i) vn[u][i] = ld_pred_f64(ck + (long long)i * B, ok);
     }
   };
   load_v(C - 1);

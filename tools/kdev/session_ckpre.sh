@@ -1,0 +1,22 @@
+#!/bin/bash
+# A/B: checkpoints by predicated loads a chunk ahead (twisted: newly a chunk ahead) vs the previous build
+out=gpurun_out/ab_ckpre.log
+: > $out
+for rep in 1 2; do
+  for lib in libwhit.so libwhit_old.so; do
+    for qb in 8192 16384; do
+      for cfg in hetero homo; do
+        echo "### $lib $cfg B=$qb rep=$rep" >> $out
+        WHIT_LIB_PATH=$PWD/paper_2604_00048_b200/$lib QT_B=$qb timeout 300 python tools/quick_time.py $cfg >> $out 2>&1
+      done
+    done
+    echo "### $lib homo rep=$rep" >> $out
+    WHIT_LIB_PATH=$PWD/paper_2604_00048_b200/$lib timeout 300 python tools/quick_time.py homo >> $out 2>&1
+  done
+done
+bash tools/kdev/gpu_ab.sh $out libwhit.so libwhit_old.so libwhit.so libwhit_old.so -- --op irregular --steps 20 --warmup 5 --no-e2e
+bash tools/kdev/gpu_ab.sh $out libwhit.so libwhit_old.so libwhit.so libwhit_old.so -- --op table1 --steps 20 --warmup 5 --no-e2e
+bash tools/kdev/gpu_ab.sh $out libwhit.so libwhit_old.so libwhit.so libwhit_old.so -- --op variance --steps 20 --warmup 5 --no-e2e
+bash tools/kdev/gpu_ab.sh $out libwhit.so libwhit_old.so libwhit.so libwhit_old.so -- --config s2tile --steps 10 --warmup 3 --no-e2e
+python -m pytest tests -q -m gpu -x -k "twist or irregular or times or variance or bands or guard or status" > gpurun_out/ckpre_tests.log 2>&1
+tail -2 gpurun_out/ckpre_tests.log
