@@ -407,9 +407,10 @@ int tw_split(const whit_ws* ws) { return ws->kk * int((ws->T - ws->d) / (2 * ws-
 
 // Small batches take the twisted path: a warp group's 32 series are split in time between two warps, which
 // halves the per-series latency and doubles the warps in flight.  It wins while its 2 x B/32 warps fit one
-// wave of 12 warps on each of the 148 SMs (B <= 28,416: 1.85x at B = 8,192, 1.6x at 16,384); beyond that a
-// twisted tail wave costs more than it saves (profiles/r2_twist_sweep.log).  WHIT_TWIST=0 never,
-// =1 whenever the shape allows; whit_ws_set_twist overrides both per workspace.
+// wave of 12 warps on each of the 148 SMs -- scalar lambda: B <= 28,416 (8,192: 1.0 -> 1.9x); per-date lambda,
+// whose sequential kernel fills that wave better: B <= 24,864 (at 28,416 the sequential kernel is 5 % faster);
+// beyond that a twisted tail wave costs more than it saves (profiles/r2_twist_tune.log).
+// WHIT_TWIST=0 never, =1 whenever the shape allows; whit_ws_set_twist overrides both per workspace.
 bool tw_pick(const whit_ws* ws) {
   if (ws->nb != 1 || ws->irr) return false;
   const int m = tw_split(ws);
@@ -421,7 +422,7 @@ bool tw_pick(const whit_ws* ws) {
   const int mode = ws->tw_mode == 2 ? 0 : ws->tw_mode >= 0 ? ws->tw_mode : env_mode;
   if (mode == 0) return false;
   if (mode == 1) return true;
-  return ws->B <= 148LL * 12 * 16;
+  return ws->B <= 148LL * 12 * (ws->lm == WHIT_LAMBDA_PER_DATE ? 14 : 16);
 }
 
 // Hybrid launch for batches just past one wave of whit_kernel (1,776 < G <= 2,400 groups of 32, e.g. homo's
