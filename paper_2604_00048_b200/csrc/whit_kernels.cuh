@@ -427,6 +427,15 @@ template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = fa
   static constexpr uint32_t BYTES_DN = ((WB ? 1 : 2) * K + (PD ? K + D : 0) + (BWD ? K : 0) + (LOSS ? K : 0)) * ROW;
 };
 
+// Shared memory per warp of a whit_kernel instantiation: the plain backward also hosts the bit-packed body
+// (warps whose forward found W binary), whose ring may be deeper (WHIT_BWD_WB_ST) -- the larger of the two.
+template <int D, typename IO, bool PD, bool BWD, bool LOSS, bool WB> struct WarpAlloc {
+  static constexpr int a = Layout<D, IO, PD, BWD, LOSS, WB>::WARP_SMEM;
+  static constexpr int b = (BWD && !WB && !LOSS) ? Layout<D, IO, PD, BWD, LOSS, true>::WARP_SMEM : 0;
+  static constexpr int value = a > b ? a : b;
+  static constexpr int smem = Layout<D, IO, PD, BWD, LOSS, WB>::WARPS * value;
+};
+
 // Issue tile i (up sweep tiles 0..C-1, then down sweep C-1..0) of one warp.
 // skip_w (binary W detected, WD): the tile's w rows are not loaded -- the consumer reads the bit plane.
 template <int D, typename IO, bool PD, bool BWD, bool LOSS = false, bool WB = false>
@@ -944,7 +953,6 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   static_assert(!LOSS || !BWD, "the fused loss is a forward variant");
   static_assert(!WB || !LOSS, "bit-packed W is a fwd/bwd variant");
   using L = Layout<D, IO, PD, BWD, LOSS, WB>;
-  static_assert(!BWD || WB || Layout<D, IO, PD, BWD, LOSS, true>::WARP_SMEM <= L::WARP_SMEM, "bits body ring");
   extern __shared__ __align__(1024) unsigned char smem[];
   // mbarriers: enough for the bit-packed backward body's ring too (WHIT_BWD_WB_ST)
   constexpr int NBAR = Layout<D, IO, PD, BWD, LOSS, true>::ST > L::ST ? Layout<D, IO, PD, BWD, LOSS, true>::ST : L::ST;
@@ -954,7 +962,7 @@ __global__ void __maxnreg__((LOSS ? 200 : Tile<IO, D, BWD>::MAXREG)) whit_kernel
   if (bw >= p.B) return;  // past the end; no barrier follows for these warps
   if (p.g_hi > 0 && (bw >> 5) >= p.g_hi) return;       // hybrid: the twisted kernel's groups
   if (p.tw_filter && p.twflag[bw >> 5] != 0) return;  // solved by the twisted kernel
-  unsigned char* ring = smem + warp * L::WARP_SMEM;
+  unsigned char* ring = smem + warp * WarpAlloc<D, IO, PD, BWD, LOSS, WB>::value;
   if constexpr (BWD && !WB && !LOSS) {
     if (p.wflag != nullptr && p.wflag[bw >> 5] != 0) {
       whit_body<D, IO, PD, BWD, LOSS, true>(p, ring, full_bar[warp], lane, bw, true);

@@ -65,15 +65,16 @@ inline whit_status launch_error(const char* what) {
 template <int D, typename IO, bool PD, bool BWD, bool LOSS, bool WB>
 whit_status launch(const whit::Params& p, cudaStream_t s) {
   using L = whit::Layout<D, IO, PD, BWD, LOSS, WB>;
-  static_assert(L::SMEM <= kSmemBudget, "CTA shared memory over budget");
+  constexpr int SMEM = whit::WarpAlloc<D, IO, PD, BWD, LOSS, WB>::smem;
+  static_assert(SMEM <= kSmemBudget, "CTA shared memory over budget");
   constexpr auto K = whit::whit_kernel<D, IO, PD, BWD, LOSS, WB>;
-  const cudaError_t ae = ensure_smem_attr<K>(L::SMEM);
+  const cudaError_t ae = ensure_smem_attr<K>(SMEM);
   if (ae != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ae));
   // one series per thread, one TMA pipeline per warp (hybrid: only the CTAs of groups [0, g_hi))
   const int threads = 32 * L::WARPS;
   const long long nser = p.g_hi > 0 && 32LL * p.g_hi < p.B ? 32LL * p.g_hi : p.B;
   const long long grid = (nser + threads - 1) / threads;
-  K<<<dim3((unsigned)grid), dim3(threads), L::SMEM, s>>>(p);
+  K<<<dim3((unsigned)grid), dim3(threads), SMEM, s>>>(p);
   return launch_error("kernel launch");
 }
 
