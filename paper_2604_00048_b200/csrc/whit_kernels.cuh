@@ -272,9 +272,13 @@ template <int D> __device__ __forceinline__ void state_init(FState<D>& s) {
 template <int D, int NEWTON>
 __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, double b, double (&A)[D],
                                          double& Dt, double& idt, double& vt) {
-  double E[D + 1];
+  // A[t][j] = c_j / D_{t-j} with c_j the deviation-form numerator; the j = 1 term of the new pivot is
+  // summed as (c_1 * inner_1) / D_{t-1} (fma with the reciprocal last), so the loop-carried chain from the
+  // previous row's reciprocal to this row's pivot is one fma instead of a multiply and an fma
+  double E[D + 1], c[D];
   E[D] = 0.0;
-  A[D - 1] = (-Mj(D, D) * s.dl[D - 1]) * s.id[D - 1];
+  c[D - 1] = -Mj(D, D) * s.dl[D - 1];
+  A[D - 1] = c[D - 1] * s.id[D - 1];
 #pragma unroll
   for (int m = D - 1; m >= 1; --m) {
     // j = D term (E_D = 0): - M_D lam~[t-D] A[t-m][D-m]
@@ -287,7 +291,8 @@ __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, d
       e = fma(-Mj(D, j - m), E[j], e);
     }
     E[m] = e;
-    A[m - 1] = fma(-Mj(D, m), s.dl[m - 1], e) * s.id[m - 1];
+    c[m - 1] = fma(-Mj(D, m), s.dl[m - 1], e);
+    A[m - 1] = c[m - 1] * s.id[m - 1];
   }
   double dl = w;
 #pragma unroll
@@ -295,7 +300,7 @@ __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, d
 #pragma unroll
   for (int j = D; j >= 1; --j) {
     const double inner = (j < D) ? fma(Mj(D, j), s.lm[j - 1], E[j]) : Mj(D, j) * s.lm[j - 1];
-    dl = fma(-A[j - 1], inner, dl);
+    dl = (j > 1) ? fma(-A[j - 1], inner, dl) : fma(-s.id[0], c[0] * inner, dl);
   }
   Dt = lam_t + dl;
   idt = rcp64<NEWTON>(Dt);
@@ -1029,9 +1034,10 @@ __device__ __forceinline__ void ldl_step_irr(IState<D>& S, const double (&mu_t)[
                                              double b, double (&A)[D], double& Dt, double& idt, double& vt) {
   FState<D>& s = S.f;
   // Mt[j] = M~[t][t-j] = mu_{t-j}[j] = S.mu[j-1][j-1];  Mm(m, j) = M~[t-m][t-j] = S.mu[j-1][j-m-1]
-  double E[D + 1];
+  double E[D + 1], c[D];  // (the j = 1 term with the reciprocal last, as ldl_step)
   E[D] = 0.0;
-  A[D - 1] = (-S.mu[D - 1][D - 1] * s.dl[D - 1]) * s.id[D - 1];
+  c[D - 1] = -S.mu[D - 1][D - 1] * s.dl[D - 1];
+  A[D - 1] = c[D - 1] * s.id[D - 1];
 #pragma unroll
   for (int m = D - 1; m >= 1; --m) {
     double e = (-(S.mu[D - 1][D - 1] * s.lm[D - 1])) * s.ap[m - 1][D - m - 1];
@@ -1043,7 +1049,8 @@ __device__ __forceinline__ void ldl_step_irr(IState<D>& S, const double (&mu_t)[
       e = fma(-S.mu[j - 1][j - m - 1], E[j], e);
     }
     E[m] = e;
-    A[m - 1] = fma(-S.mu[m - 1][m - 1], s.dl[m - 1], e) * s.id[m - 1];
+    c[m - 1] = fma(-S.mu[m - 1][m - 1], s.dl[m - 1], e);
+    A[m - 1] = c[m - 1] * s.id[m - 1];
   }
   double dl = w;
 #pragma unroll
@@ -1051,7 +1058,7 @@ __device__ __forceinline__ void ldl_step_irr(IState<D>& S, const double (&mu_t)[
 #pragma unroll
   for (int j = D; j >= 1; --j) {
     const double inner = (j < D) ? fma(S.mu[j - 1][j - 1], s.lm[j - 1], E[j]) : S.mu[j - 1][j - 1] * s.lm[j - 1];
-    dl = fma(-A[j - 1], inner, dl);
+    dl = (j > 1) ? fma(-A[j - 1], inner, dl) : fma(-s.id[0], c[0] * inner, dl);
   }
   Dt = lam_t + dl;
   idt = rcp64<NEWTON>(Dt);
