@@ -626,9 +626,13 @@ struct Sweep {
     const int t = t0 + k;
     double z = qk;
 #pragma unroll
-    for (int j = D; j >= 1; --j) {  // z[t+1] (just computed) enters last
-      z = fma(-Mj(D, j), zw[j - 1], z);
-      z = fma(-win[j - 1][j - 1], zw[j - 1], z);
+    for (int j = D; j >= 1; --j) {  // z[t+1] (just computed) enters last, with L = M + A summed first:
+      if (j > 1) {                   // one fma on the loop-carried chain (every kernel family alike)
+        z = fma(-Mj(D, j), zw[j - 1], z);
+        z = fma(-win[j - 1][j - 1], zw[j - 1], z);
+      } else {
+        z = fma(-(Mj(D, 1) + win[0][0]), zw[0], z);
+      }
     }
     // (D z)_t = sum_j c_j z[t+j]  (rows t <= T-d-1)
     double dz = Cj(D, 0) * z;
@@ -1322,8 +1326,12 @@ __global__ void __maxnreg__((D == 3 ? 224 : 168)) whit_irr_kernel(const __grid_c
   #pragma unroll
         for (int j = D; j >= 1; --j) {
           const double a = (k + j < K) ? Ak[k + j][j - 1] : cA[k + j - K][j - 1];
-          z = fma(-Mk[k][j - 1], zw[j - 1], z);
-          z = fma(-a, zw[j - 1], z);
+          if (j > 1) {
+            z = fma(-Mk[k][j - 1], zw[j - 1], z);
+            z = fma(-a, zw[j - 1], z);
+          } else {
+            z = fma(-(Mk[k][0] + a), zw[0], z);  // (L = M~ + A first, as Sweep::back_row)
+          }
         }
         // (D z)_t = c_{t,0} (z_t + sum_j mu_t[j] z_{t+j})
         double u = z;

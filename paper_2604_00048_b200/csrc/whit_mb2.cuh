@@ -520,9 +520,14 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
         for (int u = 0; u < BPW; ++u) {
           double z = q[u][k];
 #pragma unroll
-          for (int j = D; j >= 1; --j) {  // M~[t+j][t] = mu_t[j] (IRR), else M_j
-            z = fma(-(IRR ? FMU[((k + D) * D + j - 1) * 32] : Mj(D, j)), zw[u][j - 1], z);
-            z = fma(-a[j - 1], zw[u][j - 1], z);
+          for (int j = D; j >= 1; --j) {  // M~[t+j][t] = mu_t[j] (IRR), else M_j; j = 1: L = M + A first
+            const double mj = IRR ? FMU[((k + D) * D + j - 1) * 32] : Mj(D, j);
+            if (j > 1) {
+              z = fma(-mj, zw[u][j - 1], z);
+              z = fma(-a[j - 1], zw[u][j - 1], z);
+            } else {
+              z = fma(-(mj + a[0]), zw[u][0], z);
+            }
           }
           double dz;
           if constexpr (IRR) {  // (D z)_t = c_{t,0} (z_t + sum_j mu_t[j] z_{t+j})

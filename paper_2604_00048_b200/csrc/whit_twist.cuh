@@ -138,8 +138,12 @@ struct TwSweep {
 #pragma unroll
       for (int j = D; j >= 1; --j) {
         const double a = (p + j < K) ? Ak[p + j][j - 1] : cA[p + j - K][j - 1];
-        z = fma(-Mj(D, j), zw[j - 1], z);
-        z = fma(-a, zw[j - 1], z);
+        if (j > 1) {
+          z = fma(-Mj(D, j), zw[j - 1], z);
+          z = fma(-a, zw[j - 1], z);
+        } else {
+          z = fma(-(Mj(D, 1) + a), zw[0], z);  // (L = M + A first, as Sweep::back_row)
+        }
       }
       if (EDGE && t >= m && t < m + D) {
         // S row: the twist solution (select, no dynamic register indexing)
