@@ -304,11 +304,15 @@ __device__ __forceinline__ void ldl_step(FState<D>& s, double w, double lam_t, d
   }
   Dt = lam_t + dl;
   idt = rcp64<NEWTON>(Dt);
-  double v = b;
+  double v = b;  // forward substitution; the j = 1 term with L = M + A summed first (as the back substitution)
 #pragma unroll
   for (int j = D; j >= 1; --j) {
-    v = fma(-Mj(D, j), s.v[j - 1], v);
-    v = fma(-A[j - 1], s.v[j - 1], v);
+    if (j > 1) {
+      v = fma(-Mj(D, j), s.v[j - 1], v);
+      v = fma(-A[j - 1], s.v[j - 1], v);
+    } else {
+      v = fma(-(Mj(D, 1) + A[0]), s.v[0], v);
+    }
   }
   vt = v;
   // advance
@@ -1066,11 +1070,15 @@ __device__ __forceinline__ void ldl_step_irr(IState<D>& S, const double (&mu_t)[
   }
   Dt = lam_t + dl;
   idt = rcp64<NEWTON>(Dt);
-  double v = b;
+  double v = b;  // (the j = 1 term with L = M~ + A summed first, as ldl_step)
 #pragma unroll
   for (int j = D; j >= 1; --j) {
-    v = fma(-S.mu[j - 1][j - 1], s.v[j - 1], v);
-    v = fma(-A[j - 1], s.v[j - 1], v);
+    if (j > 1) {
+      v = fma(-S.mu[j - 1][j - 1], s.v[j - 1], v);
+      v = fma(-A[j - 1], s.v[j - 1], v);
+    } else {
+      v = fma(-(S.mu[0][0] + A[0]), s.v[0], v);
+    }
   }
   vt = v;
 #pragma unroll

@@ -388,8 +388,13 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
           double vv = rhs_times_w<IO, BWD>(t_rhs[(u * K + k) * 32], wio, w);
 #pragma unroll
           for (int j = D; j >= 1; --j) {  // M~[t][t-j] = mu_{t-j}[j] (IRR), else M_j
-            vv = fma(-(IRR ? FMU[((k + D - j) * D + j - 1) * 32] : Mj(D, j)), v[u][j - 1], vv);
-            vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
+            const double mj = IRR ? FMU[((k + D - j) * D + j - 1) * 32] : Mj(D, j);
+            if (j > 1) {
+              vv = fma(-mj, v[u][j - 1], vv);
+              vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
+            } else {  // (L = M + A first, as ldl_step)
+              vv = fma(-(mj + FA[k * D * 32]), v[u][0], vv);
+            }
           }
 #pragma unroll
           for (int i = D - 1; i >= 1; --i) v[u][i] = v[u][i - 1];
@@ -489,8 +494,13 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
         double vv = rhs_times_w<IO, BWD>(t_rhs[(u * K + k) * 32], wio, w);
 #pragma unroll
         for (int j = D; j >= 1; --j) {
-          vv = fma(-(IRR ? FMU[((k + D - j) * D + j - 1) * 32] : Mj(D, j)), v[u][j - 1], vv);
-          vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
+          const double mj = IRR ? FMU[((k + D - j) * D + j - 1) * 32] : Mj(D, j);
+          if (j > 1) {
+            vv = fma(-mj, v[u][j - 1], vv);
+            vv = fma(-FA[(k * D + j - 1) * 32], v[u][j - 1], vv);
+          } else {
+            vv = fma(-(mj + FA[k * D * 32]), v[u][0], vv);
+          }
         }
 #pragma unroll
         for (int i = D - 1; i >= 1; --i) v[u][i] = v[u][i - 1];

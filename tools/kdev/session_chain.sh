@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B: the loop-carried chains (factor recurrence, back substitution) shortened by one op vs the previous build
-out=gpurun_out/ab_chain2.log
+out=gpurun_out/ab_chain3.log
 : > $out
 for rep in 1 2; do
   for lib in libwhit.so libwhit_old.so; do
@@ -19,5 +19,5 @@ done
 bash tools/kdev/gpu_ab.sh $out libwhit.so libwhit_old.so libwhit.so libwhit_old.so -- --op table1 --steps 20 --warmup 5 --no-e2e
 bash tools/kdev/gpu_ab.sh $out libwhit.so libwhit_old.so libwhit.so libwhit_old.so -- --config s2tile --steps 10 --warmup 3 --no-e2e
 bash tools/kdev/gpu_ab.sh $out libwhit.so libwhit_old.so -- --op irregular --steps 20 --warmup 5 --no-e2e
-python -m pytest tests -q -m gpu > gpurun_out/chain2_tests.log 2>&1
-tail -3 gpurun_out/chain2_tests.log
+python -m pytest tests -q -m gpu > gpurun_out/chain3_tests.log 2>&1
+tail -3 gpurun_out/chain3_tests.log
