@@ -32,7 +32,9 @@ def _worker(rank, world, port, q):
     dist.all_gather_object(gathered, (off, B, {k: x[k].clone() for k in ("y", "w", "lam", "g")}))
     cks = bench.gather_checksums((x["y"], x["lam"]), world)
     if rank == 0:
-        q.put((mx, gathered, cks))
+        # numpy copies through the queue: a torch tensor would travel as a shared-memory handle that the
+        # parent may only open after this process has exited (and the segment with it)
+        q.put((mx, [(o, n, {k: v.numpy().copy() for k, v in t.items()}) for o, n, t in gathered], cks))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -49,7 +51,7 @@ def test_world2_shards_timing_and_rank_independent_inputs():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert mx == 2.5
-    (o0, b0, x0), (o1, b1, x1) = gathered
+    (o0, b0, x0), (o1, b1, x1) = [(o, n, {k: torch.from_numpy(v) for k, v in t.items()}) for o, n, t in gathered]
     assert (o0, b0, o1, b1) == (0, 64, 64, 64)  # contiguous, disjoint, covering [0, 128)
     import synth
     full = synth.make_inputs("hetero", B=128, T=80)
