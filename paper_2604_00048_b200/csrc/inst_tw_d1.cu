@@ -3,8 +3,10 @@
 #include "whit_launch.cuh"
 namespace whit_detail {
 #define WHIT_INST(IO, PD)                                                                  \
-  template whit_status launch_tw<1, IO, PD, false>(const whit::Params&, cudaStream_t); \
-  template whit_status launch_tw<1, IO, PD, true>(const whit::Params&, cudaStream_t);
+  template whit_status launch_tw<1, IO, PD, false, false>(const whit::Params&, cudaStream_t); \
+  template whit_status launch_tw<1, IO, PD, true, false>(const whit::Params&, cudaStream_t);  \
+  template whit_status launch_tw<1, IO, PD, false, true>(const whit::Params&, cudaStream_t);  \
+  template whit_status launch_tw<1, IO, PD, true, true>(const whit::Params&, cudaStream_t);
 WHIT_INST(float, true)
 WHIT_INST(float, false)
 WHIT_INST(double, true)

@@ -512,22 +512,35 @@ whit_status tw_fill(const whit_ws* ws, Params* p, const void* rhs, const void* w
   return WHIT_OK;
 }
 
-template <typename IO, bool PD, bool BWD>
+template <typename IO, bool PD, bool BWD, bool HIREG>
 whit_status dispatch_tw_d(int d, const Params& p, cudaStream_t s) {
   switch (d) {
-    case 1: return whit_detail::launch_tw<1, IO, PD, BWD>(p, s);
-    case 2: return whit_detail::launch_tw<2, IO, PD, BWD>(p, s);
-    case 3: return whit_detail::launch_tw<3, IO, PD, BWD>(p, s);
+    case 1: return whit_detail::launch_tw<1, IO, PD, BWD, HIREG>(p, s);
+    case 2: return whit_detail::launch_tw<2, IO, PD, BWD, HIREG>(p, s);
+    case 3: return whit_detail::launch_tw<3, IO, PD, BWD, HIREG>(p, s);
   }
   return fail(WHIT_ERR_ARG, "d must be 1, 2 or 3");
 }
 
-template <bool BWD>
-whit_status dispatch_tw(const whit_ws* ws, const Params& p) {
+// Twisted launches of at most one wave at 8 warps/SM (148 x 4 warp pairs = 592 groups of 32 series) take the
+// 255-register build: no spills, and the lower occupancy costs nothing there (homo-shaped 8,192 series:
+// 11.9 -> 13.8 M series/s, 16,384: 20.3 -> 23.6 M; at 24,576 the 168-register build is faster, 23.4 vs 18.8).
+constexpr long long kTwHiregGroups = 148LL * 4;
+
+template <bool BWD, bool HIREG>
+whit_status dispatch_tw_r(const whit_ws* ws, const Params& p) {
   const bool pd = ws->lm == WHIT_LAMBDA_PER_DATE;
   if (ws->dt == WHIT_F32)
-    return pd ? dispatch_tw_d<float, true, BWD>(ws->d, p, ws->stream) : dispatch_tw_d<float, false, BWD>(ws->d, p, ws->stream);
-  return pd ? dispatch_tw_d<double, true, BWD>(ws->d, p, ws->stream) : dispatch_tw_d<double, false, BWD>(ws->d, p, ws->stream);
+    return pd ? dispatch_tw_d<float, true, BWD, HIREG>(ws->d, p, ws->stream)
+              : dispatch_tw_d<float, false, BWD, HIREG>(ws->d, p, ws->stream);
+  return pd ? dispatch_tw_d<double, true, BWD, HIREG>(ws->d, p, ws->stream)
+            : dispatch_tw_d<double, false, BWD, HIREG>(ws->d, p, ws->stream);
+}
+
+template <bool BWD>
+whit_status dispatch_tw(const whit_ws* ws, const Params& p) {
+  const long long groups = (ws->B + 31) / 32 - 2LL * p.tw_cta0;  // (hybrid: the groups past the sequential part)
+  return groups <= kTwHiregGroups ? dispatch_tw_r<BWD, true>(ws, p) : dispatch_tw_r<BWD, false>(ws, p);
 }
 
 }  // namespace

@@ -33,8 +33,8 @@ whit_status launch_var(const whit::Params& p, cudaStream_t s);
 // Single-series irregular-grid kernel (NEXT-2).
 template <int D, typename IO, bool PD, bool BWD>
 whit_status launch_irr(const whit::Params& p, cudaStream_t s);
-// Twisted (two-ended) single-series kernel for small batches (whit_twist.cuh).
-template <int D, typename IO, bool PD, bool BWD>
+// Twisted (two-ended) single-series kernel for small batches (whit_twist.cuh); HIREG: the 255-register build.
+template <int D, typename IO, bool PD, bool BWD, bool HIREG = false>
 whit_status launch_tw(const whit::Params& p, cudaStream_t s);
 
 #ifdef WHIT_LAUNCH_DEFS
@@ -116,11 +116,11 @@ whit_status launch_irr(const whit::Params& p, cudaStream_t s) {
   K<<<dim3((unsigned)grid), dim3((unsigned)per_cta), L::SMEM, s>>>(p);
   return launch_error("kernel launch");
 }
-template <int D, typename IO, bool PD, bool BWD>
+template <int D, typename IO, bool PD, bool BWD, bool HIREG>
 whit_status launch_tw(const whit::Params& p, cudaStream_t s) {
   using L = whit::TwLayout<D, IO, PD, BWD>;
   static_assert(L::SMEM <= kSmemBudget, "CTA shared memory over budget");
-  constexpr auto K = whit::whit_tw_kernel<D, IO, PD, BWD>;
+  constexpr auto K = whit::whit_tw_kernel<D, IO, PD, BWD, HIREG>;
   const cudaError_t ae = ensure_smem_attr<K>(L::SMEM);
   if (ae != cudaSuccess) return fail(WHIT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(ae));
   const long long per_cta = 32 * L::PAIRS;  // series per CTA (two warps per 32 series)

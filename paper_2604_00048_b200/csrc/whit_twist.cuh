@@ -501,8 +501,11 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
   }
 }
 
-template <int D, typename IO, bool PD, bool BWD>
-__global__ void __maxnreg__(WHIT_TW_MAXREG) whit_tw_kernel(const __grid_constant__ Params p) {
+// HIREG: the instantiation for launches whose warps fit one wave at 8 warps/SM (<= 592 groups): 255
+// registers, no spills (the 168-register build spills up to 360 B at d = 3 and keeps 12 warps/SM, which only
+// pays once the twisted warps fill that wave)
+template <int D, typename IO, bool PD, bool BWD, bool HIREG = false>
+__global__ void __maxnreg__((HIREG ? 255 : WHIT_TW_MAXREG)) whit_tw_kernel(const __grid_constant__ Params p) {
   using L = TwLayout<D, IO, PD, BWD>;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t full_bar[2 * L::PAIRS][L::ST];
