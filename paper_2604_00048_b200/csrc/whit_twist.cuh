@@ -213,7 +213,7 @@ __device__ __forceinline__ void tw_issue(const Params& p, unsigned char* stage, 
   }
 }
 
-template <int D, typename IO, bool PD, bool BWD, bool REV>
+template <int D, typename IO, bool PD, bool BWD, bool REV, bool HIREG>
 __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, uint64_t* bars, double* xme,
                                         const double* xother, int pair_bar, int lane, long long bw, bool valid,
                                         long long b, double lam_s) {
@@ -399,9 +399,9 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
   }
   double lam_acc = 0.0;
   // checkpoints of the next chunk, loaded one chunk ahead by predicated loads (ld_pred_f64): 8,192 hetero series
-  // 0.72 -> 0.61 ms per fwd+bwd step.  Not in the scalar-lambda forward, where the prefetch registers spill
-  // (its chunk then waits on its own checkpoint load, as before: 0.348 vs 0.363 ms)
-  constexpr bool CKPRE = PD || BWD;
+  // 0.72 -> 0.61 ms per fwd+bwd step.  Not in the 168-register scalar-lambda forward, where the prefetch registers
+  // spill (its chunk then waits on its own checkpoint load, as before: 0.348 vs 0.363 ms)
+  constexpr bool CKPRE = PD || BWD || HIREG;
   double pck[NFAC], pv[D];
   auto load_ck = [&](int c) {
     const double* ckf = p.ck_fac + (long long)(slot0 + c) * NFAC * B + b;
@@ -530,9 +530,9 @@ __global__ void __maxnreg__((HIREG ? 255 : WHIT_TW_MAXREG)) whit_tw_kernel(const
   const int pair_bar = 1 + pair;
   if (WHIT_TW_STAGE == 1) return;
   if (half == 0)
-    tw_half<D, IO, PD, BWD, false>(p, ring, bars, xme, xother, pair_bar, lane, bw, valid, b, lam_s);
+    tw_half<D, IO, PD, BWD, false, HIREG>(p, ring, bars, xme, xother, pair_bar, lane, bw, valid, b, lam_s);
   else
-    tw_half<D, IO, PD, BWD, true>(p, ring, bars, xme, xother, pair_bar, lane, bw, valid, b, lam_s);
+    tw_half<D, IO, PD, BWD, true, HIREG>(p, ring, bars, xme, xother, pair_bar, lane, bw, valid, b, lam_s);
 }
 
 }  // namespace whit
