@@ -184,6 +184,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # wait for nvidia-smi's first sample (its start-up can outlast a short timed region), then keep only
+            # the samples taken from here on
+            t = time.time()
+            while not self.lines and time.time() - t < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
+            self.lines.clear()
         except Exception:
             self.proc = None
 
@@ -239,8 +245,7 @@ def timed_steps(launches, steps: int, warmup: int, dev, stream, clocks: bool = T
         dist.barrier()
     torch.cuda.synchronize(dev)
     if clk:
-        clk.start()
-        time.sleep(0.15)  # let the sampler attach before the timed region
+        clk.start()  # (returns once the sampler delivers samples)
     t0.record(stream)
     for i in range(steps):
         for j, (_, fn) in enumerate(launches):
