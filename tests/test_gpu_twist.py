@@ -266,3 +266,30 @@ print(json.dumps(out))
     assert out["tw"] == [3, 3], out
     for ez, ey, el in out["errs"]:
         assert ez <= 1e-10 and ey <= 1e-9 and el <= 1e-9, out["errs"]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("per_date", [True, False])
+@pytest.mark.parametrize("d", [2, 3])
+def test_twisted_both_register_builds(d, per_date, dtype):
+    """The twisted kernel has two builds: 255 registers for launches of <= 592 groups (one wave at 8 warps/SM)
+    and 168 for larger ones.  A batch of 600 groups takes the 168-register build; its first 32
+    groups, solved alone, take the 255-register one: the same arithmetic, so the results agree bit for bit;
+    and the whole batch stays close to the sequential path (as test_twisted_close_to_sequential)."""
+    T, G = 300, 600
+    B = 32 * G
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=torch.float64, mask="bernoulli",
+                          lam_mode="per_date" if per_date else "scalar")
+    big = run(x, d, dtype, 1, T, B)
+    assert big["groups"][0] == G
+    sub = {k: (x[k][..., :32] if x[k].dim() == 2 else x[k][:32]).contiguous() for k in ("y", "w", "lam", "g")}
+    small = run(sub, d, dtype, 1, T, 32)
+    assert small["groups"][0] == 1
+    for k in ("z", "ybar", "lambar"):
+        a, b = big[k][..., :32] if big[k].dim() == 2 else big[k][:32], small[k]
+        assert torch.equal(a.cpu(), b.cpu()), k
+    seq = run(x, d, dtype, 0, T, B)
+    ym = torch.where(x["w"] > 0, x["y"].abs(), torch.zeros_like(x["y"])).amax(0).to(big["z"].device)
+    dz = ((big["z"] - seq["z"]).abs().amax(0).double() / ym).max().item()
+    lim = 1e-4 if d == 3 else {torch.float32: 1e-6, torch.float64: 1e-10}[dtype]
+    assert dz <= lim, dz
