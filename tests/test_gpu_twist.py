@@ -293,3 +293,31 @@ def test_twisted_both_register_builds(d, per_date, dtype):
     dz = ((big["z"] - seq["z"]).abs().amax(0).double() / ym).max().item()
     lim = 1e-4 if d == 3 else {torch.float32: 1e-6, torch.float64: 1e-10}[dtype]
     assert dz <= lim, dz
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_homo_full_size_hybrid_launch_sampled(dtype):
+    """BASELINE configs[1] at full size (B = 65,536, T = 3,288, scalar lambda) in the launch configuration
+    bench.py times by default -- the hybrid launch (groups [0, 1,632) sequential, the 416-group tail twisted
+    with the 255-register build; the suite pins WHIT_TWIST=0, so it is forced here with set_twist(2), which
+    picks the same split): sampled series from both parts vs O1 at the BASELINE tolerances."""
+    d = 2
+    x = synth.make_inputs("homo", device="cuda")
+    T, B = x["y"].shape
+    r = run(x, d, dtype, 2, T, B)
+    assert r["nfail"] == 0
+    assert r["groups"][0] == B // 32 - 1632  # the twisted tail
+    idx = np.unique(np.concatenate([[0, 1632 * 32 - 1, 1632 * 32, B - 1],
+                                    np.linspace(0, B - 1, 6).astype(int),
+                                    np.linspace(1632 * 32, B - 1, 4).astype(int)]))
+    h = host_inputs({k: (v[:, idx] if v.dim() == 2 else v[idx]) for k, v in x.items() if k in ("y", "w", "lam", "g")})
+    tz, tg = TOL[(dtype, d)]
+    z = r["z"][:, idx].double().cpu().numpy()
+    ybar = r["ybar"][:, idx].double().cpu().numpy()
+    lambar = r["lambar"][idx].double().cpu().numpy()
+    for i, b in enumerate(idx):
+        o = O1.forward_backward(h["y"][i], h["w"][i], h["lam"][i], d, h["g"][i])
+        ym = ymax_observed(h["y"][i], h["w"][i])
+        assert np.max(np.abs(z[:, i] - o["z"].astype(float))) / ym <= tz, (b, "z")
+        assert rel_series(ybar[:, i], o["ybar"]).max() <= tg, (b, "ybar")
+        assert abs(lambar[i] - float(o["lambar"])) <= tg * abs(float(o["lambar"])), (b, "lambar")
