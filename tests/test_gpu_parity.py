@@ -1092,3 +1092,41 @@ def test_empty_batch_through_autograd(bands):
     with pytest.raises(Exception):
         P.smooth(torch.zeros(2, 4, device="cuda"), torch.ones(2, 4, device="cuda"),
                  torch.ones(4, device="cuda"), 2)
+
+
+def test_train_step_full_size_sampled():
+    """`bench.py --op train` at its benched shape (hetero: B = 262,144, T = 3,288, per-date lambda, fp32, 20 %
+    of the observed dates held out and scored): whit_forward_mse + whit_backward on sampled series vs the
+    oracle's forward, masked-MSE loss / cotangent and backward."""
+    import paper_2604_00048_b200 as P
+
+    d = 2
+    x = synth.make_inputs("hetero", device="cuda")
+    y, w, lam = x["y"], x["w"].clone(), x["lam"]
+    T, B = y.shape
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    held = (torch.rand(w.shape, device="cuda", generator=gen) < 0.2) & (w > 0)
+    w.masked_fill_(held, 0.0)
+    lw = held.to(torch.float32)
+    del held
+    ws = P.Workspace(d, T, B, torch.float32, True)
+    z, gz, loss = torch.empty_like(y), torch.empty_like(y), torch.empty(B, device="cuda")
+    P.whit_forward_mse(y, w, lam, lw, d, T, B, z, gz, loss, ws)
+    gy, gl = torch.empty_like(y), torch.empty_like(lam)
+    P.whit_backward(gz, ws, z, gy, gl)
+    assert P.whit_failures(ws) == 0
+    torch.cuda.synchronize()
+    tz, tg = TOL[(torch.float32, d)]
+    idx = _sample(B, 4)
+    h = host_inputs({k: v[:, idx] for k, v in (("y", y), ("w", w), ("lam", lam))})
+    lwh = lw[:, idx].double().cpu().numpy().T
+    zs, gzs, gys, gls = (t[:, idx].double().cpu().numpy().T for t in (z, gz, gy, gl))
+    for i, b in enumerate(idx):
+        z1, _ = O1.forward(h["y"][i], h["w"][i], h["lam"][i], d)
+        assert np.max(np.abs(zs[i] - z1.astype(float))) / ymax_observed(h["y"][i], h["w"][i]) <= tz, b
+        l1, g1 = O1.mse_loss_grad(z1, h["y"][i], lwh[i])
+        assert abs(loss[b].item() - float(l1)) <= tg * max(float(l1), 1e-300), b
+        assert rel_series(gzs[i], g1).max() <= tg, b
+        o = O1.backward(g1.astype(float), h["w"][i], h["lam"][i], d, z1)
+        assert rel_series(gys[i], o[0]).max() <= tg, b
+        assert rel_series(gls[i], o[1]).max() <= tg, b
