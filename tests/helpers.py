@@ -30,8 +30,9 @@ def ymax_observed(y, w):
     return np.max(np.where(np.asarray(w) > 0, np.abs(y), 0.0), axis=-1)
 
 
-def run_cuda(x: dict, d: int, dtype, backward: bool = True):
-    """Forward (+ backward with x['g']) through the C-ABI; returns host numpy series-major arrays."""
+def run_cuda(x: dict, d: int, dtype, backward: bool = True, twist: int | None = None):
+    """Forward (+ backward with x['g']) through the C-ABI; returns host numpy series-major arrays.
+    twist: whit_ws_set_twist mode for the workspace (None: the suite's default, WHIT_TWIST=0)."""
     import torch
 
     import paper_2604_00048_b200 as P
@@ -40,6 +41,8 @@ def run_cuda(x: dict, d: int, dtype, backward: bool = True):
     T, B = y.shape
     per_date = lam.dim() == 2
     ws = P.Workspace(d, T, B, dtype, per_date, device=y.device)
+    if twist is not None:
+        ws.set_twist(twist)
     z = torch.empty_like(y)
     P.whit_forward(y, w, lam, d, T, B, z, ws)
     out = {"z": z}

@@ -57,11 +57,13 @@ def check(res, ref, h, d, dtype, backward=True, idx=None, label=""):
     return ez.max()
 
 
-def test_toy_config_all_series():
+@pytest.mark.parametrize("twist", [0, 1])
+def test_toy_config_all_series(twist):
     """BASELINE configs[0]: 1024 series, T = 365, d = 2, scalar lambda, fwd only; every series vs O2,
-    16 series vs O1 (dense + refinement)."""
+    16 series vs O1 (dense + refinement) -- on the sequential kernel and on the twisted one, which is the path
+    the package default (and so `bench.py --config toy`) takes at this size (the 255-register build)."""
     x = synth.make_inputs("toy", device="cuda")
-    res = run_cuda(x, 2, torch.float32, backward=False)
+    res = run_cuda(x, 2, torch.float32, backward=False, twist=twist)
     h = host_inputs(x)
     assert res["nfail"] == 0
     ref = oracle_O2(h, 2)
