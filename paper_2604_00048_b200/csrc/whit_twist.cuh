@@ -54,7 +54,7 @@ struct TwLayout {
   static constexpr uint32_t BYTES = (2 * K + (PD ? K + D : 0) + (BWD ? K : 0)) * ROW;
 };
 
-#ifndef WHIT_TW_STAGE  // debug: stop after stage n (1 init, 2 first tiles, 3 up sweep, 4 exchange); 0 = full
+#ifndef WHIT_TW_STAGE  // debug: stop after stage n (1 init, 2 first tiles, 3 up sweep, 4 exchange, 5 all but the down sweep); 0 = full
 #define WHIT_TW_STAGE 0
 #endif
 #ifndef WHIT_TW_MAXREG
@@ -389,6 +389,10 @@ __device__ __forceinline__ void tw_half(const Params& p, unsigned char* ring, ui
     }
   }
 
+  if (WHIT_TW_STAGE == 5) {  // debug timing: everything but the down sweep (the group counts as solved)
+    for (int j = it; j < ntiles && j < it + ST; ++j) mbar_wait(&bars[j % ST], (uint32_t)((j / ST) & 1));
+    return;
+  }
   // ------------------------------------------------------------ down sweep (outward from S)
   double cA[D][D], zw[D];
 #pragma unroll
