@@ -426,15 +426,18 @@ bool tw_pick(const whit_ws* ws) {
 }
 
 // Hybrid launch for batches just past one wave of whit_kernel (1,776 < G <= 2,400 groups of 32, e.g. homo's
-// 2,048): the first kHybG1 groups run the sequential kernel (its wave) while the remaining groups run twisted
+// 2,048): the first g1 groups run the sequential kernel (its wave) while the remaining groups run twisted
 // on a second stream, filling the slots the first wave leaves and finishing the tail in half the latency
 // (homo 22.6 -> 23.9 M series/s in the two-stream probe, tools/kdev/hybrid_probe.py).  Auto mode only.
-constexpr int kHybG1 = 1632;  // even (two groups per twisted CTA); 144 of the 1,776 slots left to the twisted part
+// The sequential part's group count (even: two groups per twisted CTA), by lambda mode -- re-tuned once the
+// twisted tail ran the 255-register build (profiles/r2_hybrid_g1.log, M series/s at 1,632 -> here): homo
+// 65,536 26.0 -> 26.7 (1,728), hetero-shaped 65,536 25.4 -> 25.5 (1,504).
+int hyb_g1_of(const whit_ws* ws) { return ws->lm == WHIT_LAMBDA_PER_DATE ? 1504 : 1728; }
 int hyb_pick(const whit_ws* ws) {
   if (ws->nb != 1 || ws->irr) return 0;
-  if (ws->tw_mode == 2) {  // forced (tests): whenever there are groups beyond kHybG1
-    const int m = tw_split(ws);
-    return (m >= ws->kk && ws->T - m - ws->d >= ws->kk && (ws->B + 31) / 32 > kHybG1) ? kHybG1 : 0;
+  if (ws->tw_mode == 2) {  // forced (tests): whenever there are groups beyond the split
+    const int m = tw_split(ws), g1 = hyb_g1_of(ws);
+    return (m >= ws->kk && ws->T - m - ws->d >= ws->kk && (ws->B + 31) / 32 > g1) ? g1 : 0;
   }
   if (ws->tw_mode >= 0) return 0;
   const char* e = std::getenv("WHIT_TWIST");
@@ -445,11 +448,12 @@ int hyb_pick(const whit_ws* ws) {
   const int m = tw_split(ws);
   if (m < ws->kk || ws->T - m - ws->d < ws->kk) return 0;
   const long long G = (ws->B + 31) / 32;
-  static const int g1 = [] {  // WHIT_HYB_G1: the sequential part's group count (dev A/B; even)
+  static const int g1_env = [] {  // WHIT_HYB_G1: the sequential part's group count (dev A/B; even)
     const char* v = std::getenv("WHIT_HYB_G1");
     const int x = v ? std::atoi(v) : 0;
-    return (x >= 2 && x % 2 == 0) ? x : kHybG1;
+    return (x >= 2 && x % 2 == 0) ? x : 0;
   }();
+  const int g1 = g1_env ? g1_env : hyb_g1_of(ws);
   return (G > 148 * 12 && G <= hmax && G > g1) ? g1 : 0;
 }
 

@@ -149,8 +149,9 @@ def test_guard_bands_and_determinism(family, d, per_date, dtype):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("per_date", [True, False])
 def test_guard_bands_hybrid_launch(per_date, dtype):
-    """The hybrid launch (two streams; 1,664 groups: 1,632 sequential + 32 twisted) under the same guards."""
-    d, T, B = 2, 203, 1664 * 32
+    """The hybrid launch (two streams; 1,792 groups: 1,504 / 1,728 sequential + 288 / 64 twisted, per date /
+    scalar) under the same guards."""
+    d, T, B = 2, 203, 1792 * 32
     run = _family_runs("hybrid", d, dtype, per_date, T, B)
     ref, _ = run(False)
     again, _ = run(False)

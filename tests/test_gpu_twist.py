@@ -157,7 +157,7 @@ def test_twisted_status_through_fallback(d, per_date, dtype):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("per_date", [True, False])
 def test_hybrid_launch(per_date, dtype):
-    """Hybrid launch (B just past one wave): groups [0, 1632) by the sequential kernel on the workspace
+    """Hybrid launch (B just past one wave): groups [0, g1) (1,504 per date, 1,728 scalar) by the sequential kernel on the workspace
     stream, the rest twisted on a second stream.  The sequential part equals the sequential path bitwise;
     the twisted part agrees with it inside the oracle tolerance (and a failing series there still gets its
     exact status through the fallback); O1 on a sample of both parts."""
@@ -168,7 +168,7 @@ def test_hybrid_launch(per_date, dtype):
         x["lam"][61, 60000] = float("nan")  # a failing series in the twisted part: info 62
     a = run(x, d, dtype, 2, T, B)
     s = run(x, d, dtype, 0, T, B)
-    G1 = 1632 * 32
+    G1 = (1504 if per_date else 1728) * 32
     assert a["groups"][1] == B // 32 and a["groups"][0] >= (B - G1) // 32 - 1, a["groups"]
     for k in ("z", "ybar", "lambar"):
         assert torch.equal(a[k][..., :G1].nan_to_num(7.0), s[k][..., :G1].nan_to_num(7.0)), k
@@ -298,7 +298,7 @@ def test_twisted_both_register_builds(d, per_date, dtype):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_homo_full_size_hybrid_launch_sampled(dtype):
     """BASELINE configs[1] at full size (B = 65,536, T = 3,288, scalar lambda) in the launch configuration
-    bench.py times by default -- the hybrid launch (groups [0, 1,632) sequential, the 416-group tail twisted
+    bench.py times by default -- the hybrid launch (groups [0, 1,728) sequential, the 320-group tail twisted
     with the 255-register build; the suite pins WHIT_TWIST=0, so it is forced here with set_twist(2), which
     picks the same split): sampled series from both parts vs O1 at the BASELINE tolerances."""
     d = 2
@@ -306,10 +306,11 @@ def test_homo_full_size_hybrid_launch_sampled(dtype):
     T, B = x["y"].shape
     r = run(x, d, dtype, 2, T, B)
     assert r["nfail"] == 0
-    assert r["groups"][0] == B // 32 - 1632  # the twisted tail
-    idx = np.unique(np.concatenate([[0, 1632 * 32 - 1, 1632 * 32, B - 1],
+    G1 = 1728  # the scalar-lambda split (hyb_g1_of)
+    assert r["groups"][0] == B // 32 - G1  # the twisted tail
+    idx = np.unique(np.concatenate([[0, G1 * 32 - 1, G1 * 32, B - 1],
                                     np.linspace(0, B - 1, 6).astype(int),
-                                    np.linspace(1632 * 32, B - 1, 4).astype(int)]))
+                                    np.linspace(G1 * 32, B - 1, 4).astype(int)]))
     h = host_inputs({k: (v[:, idx] if v.dim() == 2 else v[idx]) for k, v in x.items() if k in ("y", "w", "lam", "g")})
     tz, tg = TOL[(dtype, d)]
     z = r["z"][:, idx].double().cpu().numpy()
