@@ -65,8 +65,13 @@ struct MB2Layout {
   static constexpr int NFB = (BWD && !PD) ? 4 : 3;
   static constexpr int OFF_BAND = OFF_FB + NFB * FBUF;
   __host__ __device__ static constexpr int nwarps(int nb) { return (nb + BPW - 1) / BPW; }
+#ifndef WHIT_MB2_RED2
+#define WHIT_MB2_RED2 1
+#endif
+  // per-date dL/dlambda partials: slots of [nw][K][32] fp64; RED2: four slots, one barrier per two chunks
+  static constexpr int RSLOTS = WHIT_MB2_RED2 ? 4 : 2;
   static constexpr int smem(int nb) {
-    return OFF_BAND + nwarps(nb) * B_WARP + (BWD && PD ? 2 * nwarps(nb) * K * 32 * 8 : 0) +
+    return OFF_BAND + nwarps(nb) * B_WARP + (BWD && PD ? RSLOTS * nwarps(nb) * K * 32 * 8 : 0) +
            (BWD && !PD ? nwarps(nb) * 32 * 8 : 0);
   }
 };
@@ -331,7 +336,7 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
   const int nbw = min(BPW, nb - cb0);  // bands of this warp (the last warp may hold fewer)
   unsigned char* ring = smem + L::OFF_BAND + bj * L::B_WARP;
   double* redw0 = reinterpret_cast<double*>(smem + L::OFF_BAND + nw * L::B_WARP);  // [2][nw][K][32] (PD bwd)
-  double* redS = redw0 + (BWD && PD ? 2 * nw * K * 32 : 0);                          // [nw][32]
+  double* redS = redw0 + (BWD && PD ? L::RSLOTS * nw * K * 32 : 0);                  // [nw][32]
   uint64_t* bars = b_full[bj];
   auto issue = [&](int i) {
     const bool up = i < C;
@@ -460,7 +465,7 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
     // TAIL: the chunk holds rows >= T - D (the last d rows have no D z row; rows >= T none at all)
     const bool tail = t0 + K > TmD;
     IO dzv[BPW][K];
-    double* const redw = redw0 + (c & 1) * nw * K * 32;
+    double* const redw = redw0 + (c & (L::RSLOTS - 1)) * nw * K * 32;
     if (BWD) {
 #pragma unroll
       for (int u = 0; u < BPW; ++u)
@@ -588,14 +593,22 @@ __global__ void __maxnreg__((D == 3 ? WHIT_MB2_MAXREG_D3 : WHIT_MB2_MAXREG)) whi
     if (lane == 0) mbar_arrive(&fac_empty[fb % L::NFB]);
     if (BWD && PD) {
       // grad_lambda_r = sum over band warps (fixed order) of their two bands' -(D u)(D z)
-      // one barrier per chunk: slot c & 1 is written again two chunks later, after every warp
-      // has passed the next chunk's barrier, i.e. finished reducing this one
-      named_bar_sync(1, 32 * nw);
-      for (int k = bj; k < K; k += nw) {
-        const int t = t0 + k;
-        double acc = 0.0;
-        for (int j = 0; j < nw; ++j) acc += redw[(j * K + k) * 32 + lane];
-        if (valid && t < TmD) out1[(long long)t * B + b] = from_f64<IO>(acc);
+      // RSLOTS = 2: one barrier per chunk (slot c & 1 is written again two chunks later, after every warp has
+      // passed the next chunk's barrier, i.e. finished reducing this one); RSLOTS = 4: one barrier per two
+      // chunks, reducing both (a slot is rewritten four chunks later, past the next pair's barrier)
+      const bool red_now = L::RSLOTS == 2 || ((C - 1 - c) & 1) == 1 || c == 0;
+      if (red_now) {
+        named_bar_sync(1, 32 * nw);
+        const int c_hi = (L::RSLOTS == 2 || ((C - 1 - c) & 1) == 0) ? c : c + 1;  // (c == 0 alone when C is odd)
+        for (int cc = c_hi; cc >= c; --cc) {
+          const double* rw = redw0 + (cc & (L::RSLOTS - 1)) * nw * K * 32;
+          for (int k = bj; k < K; k += nw) {
+            const int t = cc * K + k;
+            double acc = 0.0;
+            for (int j = 0; j < nw; ++j) acc += rw[(j * K + k) * 32 + lane];
+            if (valid && t < TmD) out1[(long long)t * B + b] = from_f64<IO>(acc);
+          }
+        }
       }
     }
     __syncwarp();
