@@ -1132,3 +1132,18 @@ def test_train_step_full_size_sampled():
         o = O1.backward(g1.astype(float), h["w"][i], h["lam"][i], d, z1)
         assert rel_series(gys[i], o[0]).max() <= tg, b
         assert rel_series(gls[i], o[1]).max() <= tg, b
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("T", [128, 8192])
+def test_sweep_extremes(T, d, dtype):
+    """BASELINE configs[4] (the sweep: d in {1, 2, 3}, T in {128 .. 8,192}) at both ends of T, iid mask,
+    per-date lambda: every series vs O2 (Algorithm 1 in long double) at the BASELINE tolerances -- the
+    longest series the sweep times, 2.5x the headline's T."""
+    B = 64
+    x = synth.make_inputs("hetero", B=B, T=T, d=d, device="cuda", dtype=dtype, mask="bernoulli", seed=500 + d)
+    res = run_cuda(x, d, dtype)
+    h = host_inputs(x)
+    assert res["nfail"] == 0 and np.all(res["info"] == 0)
+    check(res, oracle_O2(h, d), h, d, dtype, label=f"sweep T={T} d={d} {dtype}")
