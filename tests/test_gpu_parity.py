@@ -1147,3 +1147,31 @@ def test_sweep_extremes(T, d, dtype):
     h = host_inputs(x)
     assert res["nfail"] == 0 and np.all(res["info"] == 0)
     check(res, oracle_O2(h, d), h, d, dtype, label=f"sweep T={T} d={d} {dtype}")
+
+
+def test_hetero_full_size_soft_weights_sampled():
+    """The headline shape (B = 262,144, T = 3,288, per-date lambda, fp32) with SOFT weights (w in (0, 1] on the
+    observed dates, R-4): binary-W detection finds no warp binary, so every warp runs the float-W bodies at
+    full size; sampled series vs O1."""
+    import paper_2604_00048_b200 as P
+
+    d = 2
+    x = synth.make_inputs("hetero", device="cuda")
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x["w"] = (x["w"] * (0.5 + 0.5 * torch.rand(x["w"].shape, device="cuda", generator=gen))).contiguous()
+    T, B = x["y"].shape
+    ws = P.Workspace(d, T, B, torch.float32, True)
+    z, gy, gl = torch.empty_like(x["y"]), torch.empty_like(x["y"]), torch.empty_like(x["lam"])
+    P.whit_forward(x["y"], x["w"], x["lam"], d, T, B, z, ws)
+    P.whit_backward(x["g"], ws, z, gy, gl)
+    assert P.whit_failures(ws) == 0
+    assert P.whit_wbits_detected(ws)[0] == 0  # no warp read W as bits
+    idx = _sample(B, 4)
+    h = host_inputs({k: x[k][:, idx] for k in ("y", "w", "lam", "g")})
+    zs, gys, gls = (t[:, idx].double().cpu().numpy().T for t in (z, gy, gl))
+    tz, tg = TOL[(torch.float32, d)]
+    for i, b in enumerate(idx):
+        o = O1.forward_backward(h["y"][i], h["w"][i], h["lam"][i], d, h["g"][i])
+        assert np.max(np.abs(zs[i] - o["z"].astype(float))) / ymax_observed(h["y"][i], h["w"][i]) <= tz, b
+        assert rel_series(gys[i], o["ybar"]).max() <= tg, b
+        assert rel_series(gls[i], o["lambar"]).max() <= tg, b
